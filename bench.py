@@ -1,0 +1,401 @@
+"""Benchmark: Galerkin matvec throughput (basis coeffs/s) and % of HBM roofline on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--impl ours|reference]
+
+A step is one matvec y = W(X_1..X_N) c of the workload (one batch of
+seeded synthetic input).  Default workload: cfg4 of BASELINE.json (N=4 full
+cube, K+1 = 128, 2.68e8 complex128 coefficients, 4.29 GB per vector -- far
+larger than L2, so no flush is needed between steps); it is the largest
+configuration whose matvec is HBM-bound and the one sharded across GPUs in
+slabs (§8(e)).  `--workload cfg1..cfg5` measures the others.
+
+Output: ONE JSON line on rank 0 (driver contract), with `roofline`,
+`cpu_baseline` (the oracle port timed on this host), `e2e` (host buffers in,
+result back to host, through the C-ABI), `gpu_launches` and `clocks`.
+`--impl reference` times the reference algorithm (the oracle port of
+hprop's numpy path; the reference package itself cannot travel to the GPU
+box) on this host's cores for the same workload and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workload setup
+
+def build_set(hp, w):
+    return hp.build_full(w.dim, w.bound) if w.kind == "full" else hp.build_hyperbolic(w.dim, w.bound)
+
+
+def algorithmic_bytes(w, n):
+    """32 B per coefficient per vector per matvec: c read once, y written once."""
+    return 32.0 * n * w.batch
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle port)
+
+def _cpu_sample(wname: str, sample: dict):
+    """One bounded CPU sample of the workload with the oracle (hprop's numpy algorithm)."""
+    from oracle import hprop_oracle as O
+    from paper_1403_3511_b200 import workloads as W
+
+    w = W.CONFIGS[wname]
+    ap = w.approx(0.0, validate=False)
+    if w.kind == "full" and sample.get("planes"):
+        lo, hi = sample["planes"]
+        appl = O.applier_for_slab(w.dim, w.bound, lo, hi)
+        plane = (w.bound + 1) ** (w.dim - 1)
+        rng = np.random.default_rng([w.seed, 0, lo])
+        v = rng.standard_normal(appl.n) + 1j * rng.standard_normal(appl.n)
+        nvec = 1
+    elif w.kind == "full":
+        appl = O.applier_for_full(w.dim, w.bound)
+        v = W.coefficients(w)
+        nvec = 1
+    else:
+        b = sample.get("bound", w.bound)
+        ws = w.scaled(b)
+        idx = O.hyperbolic_indices(ws.dim, ws.bound)
+        appl = O.applier_for_set(idx)
+        rng = np.random.default_rng([w.seed, 0])
+        v = rng.standard_normal(appl.n) + 1j * rng.standard_normal(appl.n)
+        nvec = 1
+    return appl, ap, v, nvec
+
+
+def _cpu_worker(args):
+    wname, sample, reps = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    appl, ap, v, nvec = _cpu_sample(wname, sample)
+    times = []
+    appl.polynomial(ap.degrees, ap.coeffs, ap.halfwidth, v)  # warm-up
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        appl.polynomial(ap.degrees, ap.coeffs, ap.halfwidth, v)
+        times.append(time.perf_counter() - t0)
+    return appl.n * nvec, times
+
+
+def cpu_plan(wname: str, workers: int):
+    """Bounded sample per worker: cfg4 -> a 12-plane j1 slab (25.2M coefficients) of the real cube."""
+    if wname == "cfg4":
+        samples = [{"planes": (8 * i, 8 * i + 12)} for i in range(workers)]
+        desc = ("hprop numpy algorithm (oracle port) on 12-plane j1 slabs of the cfg4 cube "
+                "(25.2M coefficients each, one slab per worker); rate = slab coefficients / time")
+    elif wname == "cfg3":
+        samples = [{"bound": 1023}] * workers
+        desc = "oracle port on build_hyperbolic(6,1023) (611,556 coeffs, same W) -- scaled sample of cfg3"
+    elif wname == "cfg5":
+        samples = [{"bound": 255}] * workers
+        desc = "oracle port on build_hyperbolic(8,255) (239,420 coeffs, one vector, same W) -- scaled sample of cfg5"
+    else:
+        samples = [{}] * workers
+        desc = f"oracle port on the full {wname} set"
+    return samples, desc
+
+
+def run_cpu(wname: str, workers: int, reps: int):
+    samples, desc = cpu_plan(wname, workers)
+    t0 = time.perf_counter()
+    if workers == 1:
+        res = [_cpu_worker((wname, samples[0], reps))]
+    else:
+        import multiprocessing as mp
+
+        with mp.get_context("spawn").Pool(workers) as pool:
+            res = pool.map(_cpu_worker, [(wname, s, reps) for s in samples])
+    wall = time.perf_counter() - t0
+    coeffs = sum(r[0] for r in res)
+    per_rep = [max(r[1][k] for r in res) for k in range(reps)]
+    med = float(np.median(per_rep))
+    return {"value": coeffs / med, "unit": "coeffs/s", "cores": workers, "kind": "port", "sample": desc,
+            "seconds_per_rep": med, "reps": reps, "wall_s": round(wall, 1)}
+
+
+def cpu_workers_for(wname: str) -> int:
+    ncpu = os.cpu_count() or 1
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 32 << 30
+    per = {"cfg4": 9 << 30, "cfg3": 2 << 30, "cfg5": 2 << 30}.get(wname, 1 << 30)
+    return max(1, min(ncpu, int(avail * 0.6 // per)))
+
+
+# ---------------------------------------------------------------- reference arm
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    workers = cpu_workers_for(args.workload)
+    reps = max(1, args.steps)
+    base = run_cpu(args.workload, workers, reps)
+    line = {"impl": "reference", "metric": "Galerkin matvec throughput", "value": base["value"],
+            "unit": "coeffs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": base["seconds_per_rep"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, SURVEY.md §8(d))",
+            "config": {"workload": args.workload, "threads": workers},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": base["value"], "unit": "coeffs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def gpu_arm(args, rank, world, local_rank):
+    import torch
+
+    import paper_1403_3511_b200 as hp
+    from paper_1403_3511_b200 import _native as nat
+    from paper_1403_3511_b200 import workloads as W
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = W.CONFIGS[args.workload]
+    peaks, peak_kind = measured_peaks()
+    hbm = float(peaks["hbm_gbs"])
+
+    sharding = None
+    if world > 1 and w.kind == "full" and w.batch == 1:
+        from paper_1403_3511_b200 import sharding as SH
+
+        sharding = SH.SlabShard(w.dim, w.bound, rank, world, halo=w.degree)
+        s = sharding.set
+    else:
+        s = build_set(hp, w)
+    n_local = s.size
+    appl = hp.get_applier(s)
+    ap = w.approx(0.3 if w.name == "cfg4" else 0.0, validate=False)
+
+    # inputs: the seeded workload vector (rank-local part), resident in HBM
+    if sharding is not None:
+        c_host = sharding.local_coefficients(W, w)
+    else:
+        c_host = W.coefficients(w, None if w.kind == "full" else s.indices)
+    x = torch.from_numpy(c_host).to(dev)
+    y = torch.empty_like(x)
+    batch = w.batch
+    nvec_local = n_local * batch
+
+    def step_dev():
+        if sharding is not None:
+            sharding.apply_polynomial(appl, ap, x, y)
+        else:
+            appl.apply_into(ap, x, y)
+
+    for _ in range(args.warmup):
+        step_dev()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = nat.lib().hp_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            step_dev()
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = nat.lib().hp_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max = float(t)
+    ms_step = ms_max / args.steps
+    total_coeffs = (sharding.global_size if sharding is not None else n_local) * batch
+    value = total_coeffs / (ms_step * 1e-3)
+
+    # roofline of the matvec on this GPU: algorithmic bytes / step time
+    alg_bytes = algorithmic_bytes(w, n_local)
+    achieved = alg_bytes / (ms / args.steps * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": profiled_traffic(args.workload),
+                "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg_bytes,
+                "basis": "one full matvec (all its kernels) per step; 32 B/coefficient"}
+
+    # e2e: pinned host buffers in, result back to host, timed on the device
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(c_host).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        for _ in range(1):
+            x.copy_(xh, non_blocking=True)
+            step_dev()
+            yh.copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(e_steps):
+            x.copy_(xh, non_blocking=True)
+            step_dev()
+            yh.copy_(y, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / e_steps
+        if world > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ems = float(t)
+        e2e = {"value": total_coeffs / (ems * 1e-3), "unit": "coeffs/s",
+               "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
+               "d2h_bytes_per_step": int(yh.numel() * yh.element_size()), "ms_per_step": round(ems, 3),
+               "steps": e_steps, "path": "pinned host -> HBM, hp_apply_polynomial (C ABI), HBM -> pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = run_cpu(args.workload, 1, args.cpu_reps)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {"metric": "Galerkin matvec throughput", "value": value, "unit": "coeffs/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+                "higher_is_better": True, "scaling": "strong" if sharding is not None or world == 1 else "weak",
+                "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, SURVEY.md §8(d))",
+                "config": {"workload": w.name, "set": f"{w.kind} N={w.dim} bound={w.bound}", "n": total_coeffs // batch,
+                           "batch": batch, "nterms": int(ap.nterms), "halfwidth": W.HALFWIDTH,
+                           "l2": "inputs larger than L2 (no flush)" if alg_bytes / 2 > 126e6 else
+                           "working set L2-resident (not flushed)",
+                           "parallelism": f"slab-j1 x{world}" if sharding is not None else
+                           ("single" if world == 1 else f"replicas x{world}")},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
+def profiled_traffic(workload: str):
+    """dram read+write bytes per matvec from the committed ncu capture, if any."""
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(workload)
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-reps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        gpu_arm(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

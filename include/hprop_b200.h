@@ -1,0 +1,185 @@
+/*
+ * hprop_b200 -- C ABI of the B200-native matrix-free Galerkin matvec.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `hprop` 0.1.0 (/root/reference/pkg/src/hprop).  The reference is pure
+ * Python/numpy and has no FFI; its seams are the duck-typed objects listed
+ * below.  Every entry point here replaces one reference routine (cited as
+ * <module>.py:<lines>) and is bound from Python through ctypes by
+ * paper_1403_3511_b200/_native.py (see INTEGRATION.md for the binding a
+ * maintainer adds to hprop itself).
+ *
+ * Conventions
+ *  - every function returns an hp_status (0 = HP_OK); hp_last_error() gives
+ *    the message of the last failure on the calling thread;
+ *  - pointers named *_dev are device pointers owned by the caller (PyTorch
+ *    tensors on the Python side); the library only borrows them for the
+ *    duration of the call; pointers named *_host are host memory;
+ *  - `stream` is a cudaStream_t passed as void*; all device work is
+ *    stream-ordered and asynchronous unless stated otherwise;
+ *  - coefficient vectors are `batch` consecutive vectors of n scalars in the
+ *    set's canonical (lexicographic) order; dtype HP_F64 (double) or
+ *    HP_C128 (interleaved re/im doubles, i.e. numpy complex128);
+ *  - axes are 1-based as in the reference API;
+ *  - set handles are immutable after creation and may be shared by
+ *    concurrent callers that use distinct streams, outputs and workspaces
+ *    (fast_apply.py:36-37).
+ */
+#ifndef HPROP_B200_H
+#define HPROP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int hp_status;
+enum {
+  HP_OK = 0,
+  HP_ERR_VALUE = 1,     /* maps to Python ValueError   */
+  HP_ERR_RUNTIME = 2,   /* maps to Python RuntimeError */
+  HP_ERR_CUDA = 3,      /* CUDA failure                */
+  HP_ERR_NOMEM = 4,     /* workspace too small / OOM   */
+  HP_ERR_KEY = 5        /* maps to Python KeyError     */
+};
+
+enum { HP_F64 = 0, HP_C128 = 1 };
+enum { HP_KIND_FULL = 0, HP_KIND_HYPERBOLIC = 1, HP_KIND_CUSTOM = 2 };
+
+/* flags for hp_apply_polynomial */
+enum {
+  HP_ADD_OSC = 1,       /* add sum_l (j_l + 1/2) v: apply_hamiltonian (fast_apply.py:195-198) */
+  HP_REF_ORDER = 2,     /* reproduce the reference evaluation order bit for bit (fast_apply.py:110-193) */
+  HP_CHECK_FINITE = 4   /* raise HP_ERR_RUNTIME on non-finite output (fast_apply.py:316-318); synchronises */
+};
+
+typedef struct hp_set_s* hp_set_t;
+
+int hp_abi_version(void);
+const char* hp_last_error(void);
+int hp_device_count(void);
+/* number of kernels this library has launched in the process so far */
+int64_t hp_launch_count(void);
+
+/* ---- index sets (index_set.py) ------------------------------------------ */
+
+/* build_full(dim, bound) -- index_set.py:144-154.  Ordinal of j is
+ * sum_l j_l (bound+1)^(dim-l); nothing is materialised. */
+hp_status hp_set_create_full(int dim, int bound, void* stream, hp_set_t* out, int64_t* n_out);
+
+/* Slab of a full cube: planes j1 in [lo, hi) (multi-GPU shards, §8(e)).
+ * Neighbours across the slab faces are absent; j1 keeps its global value. */
+hp_status hp_set_create_slab(int dim, int bound, int lo, int hi, void* stream,
+                             hp_set_t* out, int64_t* n_out);
+
+/* build_hyperbolic(dim, bound) -- index_set.py:157-181.  Enumerated on the
+ * device by budget-count unranking, bit-exact with the reference order;
+ * neighbour tables are built by ranking j +- e_l. */
+hp_status hp_set_create_hyperbolic(int dim, int bound, void* stream, hp_set_t* out,
+                                   int64_t* n_out);
+
+/* from_indices / IndexSet(dim, bound, kind, indices) -- index_set.py:46-65,
+ * 184-214.  indices_host: n x dim, strictly lexicographically sorted,
+ * downward closed (validated by the caller, as the reference does). */
+hp_status hp_set_create_custom(int dim, int bound, const int64_t* indices_host, int64_t n,
+                               void* stream, hp_set_t* out);
+
+hp_status hp_set_info(hp_set_t s, int* dim, int* bound, int* kind, int64_t* n);
+
+/* IndexSet.indices (index_set.py:60): n x dim int64, written to device memory. */
+hp_status hp_set_indices(hp_set_t s, int64_t* out_dev, void* stream);
+
+/* IndexSet.neighbor_ordinals(axis) -- index_set.py:104-130: int64 ordinals,
+ * -1 where absent. */
+hp_status hp_neighbor_tables(hp_set_t s, int axis, int64_t* down_dev, int64_t* up_dev,
+                             void* stream);
+
+/* Ordinal of one multi-index (IndexSet.position, index_set.py:86-88);
+ * *ord_out = -1 if absent.  Host-side, no device work. */
+hp_status hp_set_position(hp_set_t s, const int64_t* index_host, int64_t* ord_out);
+
+hp_status hp_set_destroy(hp_set_t s);
+
+/* ---- matvec (fast_apply.py) --------------------------------------------- */
+
+/* PolynomialApplier.apply_coordinate / direct_op -- fast_apply.py:59-65, 273-278 */
+hp_status hp_apply_coordinate(hp_set_t s, int axis, int dtype, const void* in_dev,
+                              void* out_dev, int64_t batch, void* stream);
+
+/* cheb_of_coordinate_apply -- fast_apply.py:281-302: T_degree(X_axis/L) v */
+size_t hp_cheb_workspace_bytes(hp_set_t s, int dtype, int64_t batch);
+hp_status hp_cheb_apply(hp_set_t s, int axis, int degree, double halfwidth, int dtype,
+                        const void* in_dev, void* out_dev, int64_t batch, void* workspace_dev,
+                        size_t workspace_bytes, void* stream);
+
+/* apply_polynomial / apply_hamiltonian -- fast_apply.py:110-198.
+ * degrees_host: nterms x dim (any integer degrees >= 0), coeffs_host: nterms.
+ * axis_order_host: NULL for the defined order, else a permutation of 1..dim
+ * (first entry applied first; disables grouping, fast_apply.py:121-125). */
+size_t hp_poly_workspace_bytes(hp_set_t s, const int32_t* degrees_host, int nterms, int dtype,
+                               int64_t batch, int flags);
+hp_status hp_apply_polynomial(hp_set_t s, const int32_t* degrees_host, const double* coeffs_host,
+                              int nterms, double halfwidth, int dtype, const void* in_dev,
+                              void* out_dev, int64_t batch, int flags,
+                              const int32_t* axis_order_host, void* workspace_dev,
+                              size_t workspace_bytes, void* stream);
+
+/* apply_square_sum -- fast_apply.py:202-245 (exact restricted sum_l x_l^2) */
+hp_status hp_square_sum(hp_set_t s, int dtype, const void* in_dev, void* out_dev,
+                        int64_t batch, void* stream);
+
+/* ---- Lanczos / Magnus (krylov_propagator.py) ---------------------------- */
+
+/* One exponential Magnus step y <- exp(-i h B) y via an m-step Lanczos
+ * factorisation (krylov_propagator.py:58-104, 107-186, 215-244), entirely on
+ * the device with no host synchronisation.  scheme 0 = midpoint (B = A(t+h/2),
+ * terms set 1), 1 = gl2 (two time points, terms sets 1 and 2).
+ * A(t) = D + W_pol(t) + q * square_sum (error_lab.py:173-185) with D the
+ * oscillator diagonal.  y_dev: complex128 n (in/out).
+ * diag_dev (optional, 4 doubles): [m_eff, hermiticity_defect, breakdown_at or -1, ql_failed]. */
+size_t hp_magnus_workspace_bytes(hp_set_t s, int scheme, const int32_t* degrees1_host,
+                                 int nterms1, const int32_t* degrees2_host, int nterms2,
+                                 int krylov_steps);
+hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* degrees1_host,
+                         const double* coeffs1_host, int nterms1, const int32_t* degrees2_host,
+                         const double* coeffs2_host, int nterms2, double halfwidth,
+                         double harmonic_q, double h, int krylov_steps, int reorthogonalize,
+                         void* y_dev, double* diag_dev, void* workspace_dev,
+                         size_t workspace_bytes, void* stream);
+
+/* lanczos(matvec, v0, steps) with the polynomial Hamiltonian as matvec --
+ * krylov_propagator.py:58-104.  Outputs: basis_dev (steps x n complex128,
+ * row k = v_k), alpha_dev (steps), beta_dev (steps-1), diag_dev as above. */
+hp_status hp_lanczos(hp_set_t s, const int32_t* degrees_host, const double* coeffs_host,
+                     int nterms, double halfwidth, double harmonic_q, const void* v0_dev,
+                     int steps, int reorthogonalize, void* basis_dev, double* alpha_dev,
+                     double* beta_dev, double* diag_dev, void* workspace_dev,
+                     size_t workspace_bytes, void* stream);
+
+/* tridiag_eigh + expm_tridiag_column -- krylov_propagator.py:107-177, on the
+ * device (one thread; m <= 64).  col_dev: m complex128. */
+hp_status hp_expm_tridiag_column(const double* alpha_dev, const double* beta_dev, int m,
+                                 double tau, void* col_dev, int* status_dev, void* stream);
+
+/* tridiag_eigh -- krylov_propagator.py:107-170 on the device (one thread;
+ * m <= 48): eigenvalues ascending (stable order) into d_dev (m), eigenvectors
+ * as columns of the row-major m x m z_dev; *status_dev = 1 if QL failed to
+ * converge within 30 iterations (the reference raises RuntimeError). */
+hp_status hp_tridiag_eigh(const double* alpha_dev, const double* beta_dev, int m, double* d_dev,
+                          double* z_dev, int* status_dev, void* stream);
+
+/* ---- BLAS-1 building blocks with deterministic reductions --------------- */
+size_t hp_reduce_workspace_bytes(int64_t n);
+/* out_dev[0..1] = sum conj(a) * b  (complex128), fixed summation order */
+hp_status hp_cdot(int64_t n, const void* a_dev, const void* b_dev, double* out_dev,
+                  void* workspace_dev, void* stream);
+/* out_dev[0] = ||a||_2 (complex128 vector), fixed summation order */
+hp_status hp_cnrm2(int64_t n, const void* a_dev, double* out_dev, void* workspace_dev,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPROP_B200_H */

@@ -1,0 +1,149 @@
+// Shared definitions for the hprop_b200 CUDA library (sm_100a).
+//
+// Scalar arithmetic on the reference-order path uses explicit round-to-
+// nearest intrinsics (__dmul_rn/__dadd_rn/__dsub_rn) so that no FMA
+// contraction happens: numpy evaluates cdown*w[down] + cup*w[up] as two
+// rounded products and a rounded sum (fast_apply.py:64-65, 74-92), and the
+// device reproduces exactly that.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/hprop_b200.h"
+
+#define HP_MAXDIM 16
+#define HP_ABI 1
+
+namespace hp {
+
+void set_error(const std::string& msg);
+void count_launch();
+hp_status fail(hp_status code, const std::string& msg);
+hp_status cuda_fail(cudaError_t e, const char* what);
+
+#define HP_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return hp::cuda_fail(e_, #call); \
+  } while (0)
+
+// every kernel launch is followed by this check, which also counts it
+// (hp_launch_count(): the "gpu_launches" figure of bench.py)
+#define HP_LAUNCH_CHECK(what)                           \
+  do {                                                  \
+    hp::count_launch();                                 \
+    cudaError_t e_ = cudaGetLastError();                \
+    if (e_ != cudaSuccess) return hp::cuda_fail(e_, what); \
+  } while (0)
+
+// ---------------------------------------------------------------- scalars
+__device__ __forceinline__ double zero_of(double) { return 0.0; }
+__device__ __forceinline__ double2 zero_of(double2) { return make_double2(0.0, 0.0); }
+
+__device__ __forceinline__ double smul(double c, double x) { return __dmul_rn(c, x); }
+__device__ __forceinline__ double2 smul(double c, double2 x) {
+  return make_double2(__dmul_rn(c, x.x), __dmul_rn(c, x.y));
+}
+__device__ __forceinline__ double sadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double2 sadd(double2 a, double2 b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ double ssub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double2 ssub(double2 a, double2 b) {
+  return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+}
+__device__ __forceinline__ double sdiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double2 sdiv(double2 a, double b) {
+  return make_double2(__ddiv_rn(a.x, b), __ddiv_rn(a.y, b));
+}
+// fused (contracted) variants for the fast path
+__device__ __forceinline__ double sfma(double c, double x, double acc) { return fma(c, x, acc); }
+__device__ __forceinline__ double2 sfma(double c, double2 x, double2 acc) {
+  return make_double2(fma(c, x.x, acc.x), fma(c, x.y, acc.y));
+}
+__device__ __forceinline__ bool sfinite(double x) { return isfinite(x); }
+__device__ __forceinline__ bool sfinite(double2 x) { return isfinite(x.x) && isfinite(x.y); }
+
+template <class T>
+__device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+
+// ---------------------------------------------------------------- axis views
+// A view answers, for one axis and one ordinal: the (global) order j_l used
+// in the ladder coefficients and the ordinals of the -/+ neighbours (-1 if
+// absent).  Boxes (full cubes and j1-slabs of full cubes) use stride
+// arithmetic; every other set uses device neighbour tables.
+struct AxBox {
+  int64_t stride;  // ordinal stride of this axis
+  int side;        // local extent of this axis
+  int joff;        // global offset of local j (slab shards, axis 1 only)
+  __device__ __forceinline__ int jloc(int64_t o) const { return (int)((o / stride) % side); }
+  __device__ __forceinline__ void at(int64_t o, int& j, int64_t& dn, int64_t& up) const {
+    int jl = jloc(o);
+    j = jl + joff;
+    dn = jl > 0 ? o - stride : -1;
+    up = jl < side - 1 ? o + stride : -1;
+  }
+};
+
+struct AxTab {
+  const int32_t* down;
+  const int32_t* up;
+  const int32_t* jv;
+  __device__ __forceinline__ void at(int64_t o, int& j, int64_t& dn, int64_t& up_) const {
+    j = __ldg(jv + o);
+    dn = __ldg(down + o);
+    up_ = __ldg(up + o);
+  }
+};
+
+}  // namespace hp
+
+// The set handle (opaque to C callers).
+struct hp_set_s {
+  int dim = 0, bound = 0, kind = 0;
+  int64_t n = 0;
+  int device = 0;
+  bool boxed = false;           // full cube or slab: stride arithmetic
+  int lo = 0, hi = 0;           // slab planes along axis 1 (full: 0..bound+1)
+  int64_t stride[HP_MAXDIM] = {0};
+  int side[HP_MAXDIM] = {0};
+  // tabled sets (hyperbolic, custom)
+  int32_t* d_down[HP_MAXDIM] = {nullptr};
+  int32_t* d_up[HP_MAXDIM] = {nullptr};
+  int32_t* d_j[HP_MAXDIM] = {nullptr};
+  // hyperbolic rank tables (host copy for position(); device copy for kernels)
+  std::vector<int64_t> h_pref;  // concatenated prefix arrays
+  std::vector<int64_t> h_off;   // (depth * (budget+1) + r) -> offset into h_pref, -1 if unused
+  int64_t* d_pref = nullptr;
+  int64_t* d_off = nullptr;
+  // custom sets keep a host copy of the indices for position()
+  std::vector<int64_t> h_indices;
+
+  hp::AxBox box(int a) const {
+    hp::AxBox v;
+    v.stride = stride[a];
+    v.side = side[a];
+    v.joff = (a == 0) ? lo : 0;
+    return v;
+  }
+  hp::AxTab tab(int a) const {
+    hp::AxTab v;
+    v.down = d_down[a];
+    v.up = d_up[a];
+    v.jv = d_j[a];
+    return v;
+  }
+};
+
+namespace hp {
+inline int grid_for(int64_t n, int block, int max_blocks = 148 * 16) {
+  int64_t g = (n + block - 1) / block;
+  if (g > max_blocks) g = max_blocks;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace hp

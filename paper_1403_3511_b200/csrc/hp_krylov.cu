@@ -1,0 +1,589 @@
+// Lanczos / Magnus time stepping on the device (reference:
+// krylov_propagator.py:58-263, error_lab.py:154-185).
+//
+// One exponential step runs without any host synchronisation: the Lanczos
+// recurrence scalars (alpha_k, beta_k, breakdown state) live in a small
+// device struct, every reduction is a fixed-shape two-stage tree (so results
+// are bitwise reproducible run to run), breakdown (beta_k <= 1e-14,
+// krylov_propagator.py:29, 90-93) truncates the factorisation on the device,
+// and the tridiagonal eigenproblem (implicit-shift QL, :107-170) plus
+// exp(-i tau T) e_1 (:173-177) run in one device thread.  The whole step is
+// therefore a pure launch sequence (CUDA-graph capturable).
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "hp_common.cuh"
+#include "hp_program.h"
+
+#define HP_MAXM 48
+#define HP_RED_BLOCKS 592
+#define HP_RED_THREADS 256
+
+namespace hp {
+
+struct LzState {
+  double alpha[HP_MAXM];
+  double beta[HP_MAXM];
+  double2 col[HP_MAXM];
+  double2 reo[HP_MAXM];
+  double nrm0;
+  double defect;
+  double scratch;
+  int m_eff;
+  int broken;
+  int breakdown_at;
+  int ql_fail;
+};
+
+// ---------------------------------------------------------------- reductions
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+
+template <int MODE>  // 0: sum conj(a)*b (complex); 1: sum |a|^2 (re in .x)
+__global__ void __launch_bounds__(HP_RED_THREADS) k_red_partial(int64_t n, const double2* __restrict__ a,
+                                                                const double2* __restrict__ b,
+                                                                double2* __restrict__ partial) {
+  __shared__ double2 sh[HP_RED_THREADS];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 x = __ldg(a + i);
+    if (MODE == 0) {
+      double2 y = __ldg(b + i);
+      acc.x = fma(x.x, y.x, fma(x.y, y.y, acc.x));
+      acc.y = fma(x.x, y.y, fma(-x.y, y.x, acc.y));
+    } else {
+      acc.x = fma(x.x, x.x, fma(x.y, x.y, acc.x));
+    }
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = HP_RED_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = cadd(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__device__ double2 block_sum_partials(const double2* partial, int np) {
+  __shared__ double2 sh[HP_RED_THREADS];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc = cadd(acc, partial[i]);
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = HP_RED_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = cadd(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  return sh[0];
+}
+
+// what: 0 alpha_k (dot), 1 nrm0 (norm), 2 beta_k (norm + breakdown), 3 reo[k] (dot),
+//       4 write dot to out[0..1], 5 write norm to out[0]
+__global__ void __launch_bounds__(HP_RED_THREADS) k_red_final(const double2* partial, int np, LzState* st,
+                                                              int k, int what, double tol, double* out) {
+  double2 s = block_sum_partials(partial, np);
+  if (threadIdx.x != 0) return;
+  if (what == 4) { out[0] = s.x; out[1] = s.y; return; }
+  if (what == 5) { out[0] = sqrt(s.x); return; }
+  if (st->broken && k >= st->m_eff) return;
+  if (what == 0) {
+    st->alpha[k] = s.x;
+    st->defect = fmax(st->defect, fabs(s.y));
+  } else if (what == 1) {
+    st->nrm0 = sqrt(s.x);
+  } else if (what == 2) {
+    double bk = sqrt(s.x);
+    st->scratch = bk;
+    if (bk <= tol) {
+      st->broken = 1;
+      st->m_eff = k + 1;
+      st->breakdown_at = k + 1;
+    } else {
+      st->beta[k] = bk;
+    }
+  } else if (what == 3) {
+    st->reo[k] = s;
+  }
+}
+
+static hp_status reduce(int mode, int64_t n, const double2* a, const double2* b, double2* partial, LzState* st,
+                        int k, int what, double tol, double* out, cudaStream_t s) {
+  if (mode == 0) k_red_partial<0><<<HP_RED_BLOCKS, HP_RED_THREADS, 0, s>>>(n, a, b, partial);
+  else k_red_partial<1><<<HP_RED_BLOCKS, HP_RED_THREADS, 0, s>>>(n, a, nullptr, partial);
+  HP_LAUNCH_CHECK("k_red_partial");
+  k_red_final<<<1, HP_RED_THREADS, 0, s>>>(partial, HP_RED_BLOCKS, st, k, what, tol, out);
+  HP_LAUNCH_CHECK("k_red_final");
+  return HP_OK;
+}
+
+// ---------------------------------------------------------------- vector kernels
+
+// dst = src / (which == 0 ? nrm0 : beta[k])   (krylov_propagator.py:72, 95)
+__global__ void k_lz_div(int64_t n, const double2* __restrict__ src, double2* __restrict__ dst,
+                         const LzState* st, int k, int which) {
+  if (which == 1 && st->broken && k >= st->m_eff - 1) return;
+  double d = which == 0 ? st->nrm0 : st->beta[k];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = sdiv(__ldg(src + i), d);
+}
+
+// w = (w - alpha_k v_k) - beta_{k-1} v_{k-1}   (krylov_propagator.py:86)
+__global__ void k_lz_update(int64_t n, double2* __restrict__ w, const double2* __restrict__ vk,
+                            const double2* __restrict__ vprev, const LzState* st, int k) {
+  if (st->broken && k >= st->m_eff) return;
+  double al = st->alpha[k];
+  double bp = k > 0 ? st->beta[k - 1] : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 t = ssub(w[i], smul(al, __ldg(vk + i)));
+    if (k > 0) t = ssub(t, smul(bp, __ldg(vprev + i)));
+    w[i] = t;
+  }
+}
+
+// full reorthogonalisation: w -= sum_{j<=k} reo[j] v_j   (krylov_propagator.py:87-88)
+__global__ void k_lz_reorth(int64_t n, double2* __restrict__ w, const double2* __restrict__ V, const LzState* st,
+                            int k) {
+  if (st->broken && k >= st->m_eff) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = 0; j <= k; ++j) {
+      double2 c = st->reo[j];
+      double2 v = __ldg(V + (int64_t)j * n + i);
+      acc.x += c.x * v.x - c.y * v.y;
+      acc.y += c.x * v.y + c.y * v.x;
+    }
+    w[i] = ssub(w[i], acc);
+  }
+}
+
+// gl2 operator average: out = 0.5 (y1 + y2) - i gamma (z2 - z1)  (krylov_propagator.py:226-231)
+__global__ void k_gl2_combine(int64_t n, const double2* __restrict__ y1, const double2* __restrict__ y2,
+                              const double2* __restrict__ z2y1, const double2* __restrict__ z1y2, double gamma,
+                              double2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 c = ssub(__ldg(z2y1 + i), __ldg(z1y2 + i));
+    double2 h = smul(0.5, sadd(__ldg(y1 + i), __ldg(y2 + i)));
+    double2 ic = make_double2(__dsub_rn(__dmul_rn(0.0, c.x), __dmul_rn(gamma, c.y)),
+                              __dadd_rn(__dmul_rn(0.0, c.y), __dmul_rn(gamma, c.x)));
+    out[i] = ssub(h, ic);
+  }
+}
+
+// y = nrm0 * sum_{k < m_eff} col_k v_k   (krylov_propagator.py:186)
+__global__ void k_lz_combine(int64_t n, const double2* __restrict__ V, const LzState* st, double2* __restrict__ y) {
+  int m = st->m_eff;
+  double s = st->nrm0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < m; ++k) {
+      double2 c = st->col[k];
+      double2 v = __ldg(V + (int64_t)k * n + i);
+      acc.x += v.x * c.x - v.y * c.y;
+      acc.y += v.x * c.y + v.y * c.x;
+    }
+    y[i] = make_double2(s * acc.x, s * acc.y);
+  }
+}
+
+// ---------------------------------------------------------------- tridiagonal QL
+
+// implicit-shift QL with eigenvectors (krylov_propagator.py:107-170);
+// returns false on non-convergence.  d[m], e[m] (e[m-1] = 0), z[m*m] col-major z[i + j*m].
+__device__ bool ql_eigh(int m, double* d, double* e, double* z) {
+  for (int i = 0; i < m * m; ++i) z[i] = 0.0;
+  for (int i = 0; i < m; ++i) z[i + i * m] = 1.0;
+  if (m == 1) return true;
+  for (int l = 0; l < m; ++l) {
+    int it = 0;
+    while (true) {
+      int mm = l;
+      while (mm < m - 1) {
+        double dd = fabs(d[mm]) + fabs(d[mm + 1]);
+        if (fabs(e[mm]) <= 1e-14 * dd) break;
+        ++mm;
+      }
+      if (mm == l) break;
+      if (it == 30) return false;
+      ++it;
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = hypot(g, 1.0);
+      g = d[mm] - d[l] + e[l] / (g + (g >= 0 ? r : -r));
+      double s = 1.0, c = 1.0, p = 0.0;
+      bool early = false;
+      for (int i = mm - 1; i >= l; --i) {
+        double f = s * e[i];
+        double b = c * e[i];
+        r = hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {
+          d[i + 1] -= p;
+          e[mm] = 0.0;
+          early = true;
+          break;
+        }
+        s = f / r;
+        c = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * s + 2.0 * c * b;
+        p = s * r;
+        d[i + 1] = g + p;
+        g = c * r - b;
+        for (int row = 0; row < m; ++row) {
+          double zi = z[row + i * m], zi1 = z[row + (i + 1) * m];
+          z[row + (i + 1) * m] = s * zi + c * zi1;
+          z[row + i * m] = c * zi - s * zi1;
+        }
+      }
+      if (!early) {
+        d[l] -= p;
+        e[l] = g;
+        e[mm] = 0.0;
+      }
+    }
+  }
+  return true;
+}
+
+// col = Z exp(-i tau Lambda) Z[0,:]  (krylov_propagator.py:173-177)
+__device__ bool expm_col(int m, const double* alpha, const double* beta, double tau, double2* col) {
+  double d[HP_MAXM], e[HP_MAXM], z[HP_MAXM * HP_MAXM];
+  int order[HP_MAXM];
+  for (int i = 0; i < m; ++i) {
+    d[i] = alpha[i];
+    e[i] = (i < m - 1) ? beta[i] : 0.0;
+  }
+  if (!ql_eigh(m, d, e, z)) return false;
+  // stable ascending order (np.argsort kind="stable")
+  for (int i = 0; i < m; ++i) order[i] = i;
+  for (int i = 1; i < m; ++i) {
+    int t = order[i], j = i - 1;
+    while (j >= 0 && d[order[j]] > d[t]) { order[j + 1] = order[j]; --j; }
+    order[j + 1] = t;
+  }
+  double2 c[HP_MAXM];
+  for (int jj = 0; jj < m; ++jj) {
+    int j = order[jj];
+    double x = tau * d[j];
+    double sn, cs;
+    sincos(x, &sn, &cs);
+    double z0 = z[0 + j * m];
+    c[jj] = make_double2(cs * z0, -sn * z0);
+  }
+  for (int i = 0; i < m; ++i) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int jj = 0; jj < m; ++jj) {
+      double zij = z[i + order[jj] * m];
+      acc.x += zij * c[jj].x;
+      acc.y += zij * c[jj].y;
+    }
+    col[i] = acc;
+  }
+  return true;
+}
+
+__global__ void k_lz_expm(LzState* st, double tau) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (!expm_col(st->m_eff, st->alpha, st->beta, tau, st->col)) st->ql_fail = 1;
+}
+
+__global__ void k_expm_standalone(const double* alpha, const double* beta, int m, double tau, double2* col,
+                                  int* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  bool ok = expm_col(m, alpha, beta, tau, col);
+  if (status) *status = ok ? 0 : 1;
+}
+
+__global__ void k_tridiag_eigh(const double* alpha, const double* beta, int m, double* dout, double* zout,
+                               int* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double d[HP_MAXM], e[HP_MAXM], z[HP_MAXM * HP_MAXM];
+  int order[HP_MAXM];
+  for (int i = 0; i < m; ++i) {
+    d[i] = alpha[i];
+    e[i] = (i < m - 1) ? beta[i] : 0.0;
+  }
+  bool ok = ql_eigh(m, d, e, z);
+  for (int i = 0; i < m; ++i) order[i] = i;
+  for (int i = 1; i < m; ++i) {
+    int t = order[i], j = i - 1;
+    while (j >= 0 && d[order[j]] > d[t]) { order[j + 1] = order[j]; --j; }
+    order[j + 1] = t;
+  }
+  for (int j = 0; j < m; ++j) {
+    dout[j] = d[order[j]];
+    for (int i = 0; i < m; ++i) zout[i * m + j] = z[i + order[j] * m];
+  }
+  if (status) *status = ok ? 0 : 1;
+}
+
+__global__ void k_lz_init(LzState* st, int m) {
+  if (threadIdx.x != 0) return;
+  st->m_eff = m;
+  st->broken = 0;
+  st->breakdown_at = -1;
+  st->ql_fail = 0;
+  st->defect = 0.0;
+  st->nrm0 = 0.0;
+  st->scratch = 0.0;
+}
+
+__global__ void k_lz_diag(const LzState* st, double* diag, double* alpha, double* beta) {
+  if (threadIdx.x != 0) return;
+  if (diag) {
+    diag[0] = st->m_eff;
+    diag[1] = st->defect;
+    diag[2] = st->breakdown_at;
+    diag[3] = st->ql_fail ? 1.0 : 0.0;
+  }
+  if (alpha) for (int k = 0; k < st->m_eff; ++k) alpha[k] = st->alpha[k];
+  if (beta) for (int k = 0; k + 1 < st->m_eff; ++k) beta[k] = st->beta[k];
+}
+
+// ---------------------------------------------------------------- operator
+
+// A(t) v = (D + W_pol) v [+ q * square_sum v]  (error_lab.py:173-185)
+struct Hamiltonian {
+  const hp_set_s* s;
+  Program prog;
+  double halfwidth;
+  double q;
+  std::vector<Term> terms;
+};
+
+static hp_status apply_ham(const Hamiltonian& H, const double2* v, double2* y, double2* ws, size_t ws_bytes,
+                           cudaStream_t st) {
+  bool done = false;
+  hp_status rc = fullgrid_apply(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done);
+  if (rc) return rc;
+  if (!done) rc = run_program<double2>(H.s, H.prog, H.halfwidth, v, y, 1, ws, ws_bytes, st);
+  return rc;
+}
+
+__global__ void k_axpy_c2(int64_t n, double c, const double2* __restrict__ x, double2* __restrict__ acc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc[i] = sadd(acc[i], smul(c, __ldg(x + i)));
+}
+
+static hp_status apply_ham_full(const Hamiltonian& H, const double2* v, double2* y, double2* tmp, double2* ws,
+                                size_t ws_bytes, cudaStream_t st) {
+  hp_status rc = apply_ham(H, v, y, ws, ws_bytes, st);
+  if (rc) return rc;
+  if (H.q != 0.0) {
+    rc = launch_square<double2>(H.s, v, tmp, 1, st);
+    if (rc) return rc;
+    int64_t n = H.s->n;
+    k_axpy_c2<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, H.q, tmp, y);
+    HP_LAUNCH_CHECK("k_axpy_c2");
+  }
+  return HP_OK;
+}
+
+// ---------------------------------------------------------------- workspace layout
+
+struct LzLayout {
+  size_t off_state, off_partial, off_V, off_w, off_tmp, off_g, off_prog, total;
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static LzLayout lz_layout(const hp_set_s* s, int m, int scheme, size_t prog_bytes) {
+  LzLayout L;
+  size_t vec = (size_t)s->n * 16;
+  size_t o = 0;
+  L.off_state = o; o = align_up(o + sizeof(LzState));
+  L.off_partial = o; o = align_up(o + HP_RED_BLOCKS * sizeof(double2));
+  L.off_V = o; o = align_up(o + (size_t)m * vec);
+  L.off_w = o; o = align_up(o + vec);
+  L.off_tmp = o; o = align_up(o + vec);
+  L.off_g = o; o = align_up(o + (scheme == 1 ? 4 * vec : 0));
+  L.off_prog = o; o = align_up(o + prog_bytes);
+  L.total = o;
+  return L;
+}
+
+static size_t prog_bytes_for(const hp_set_s* s, const std::vector<Term>& terms) {
+  Program p = build_program(s->dim, terms, HP_ADD_OSC, nullptr);
+  size_t gen = (size_t)std::max(p.nslots, 1) * s->n * 16;
+  size_t fg = fullgrid_workspace_bytes(s, terms, HP_C128, 1, HP_ADD_OSC);
+  return std::max(gen, fg);
+}
+
+// Run the Lanczos recurrence for `steps` iterations with matvec = op.
+// V: steps x n rows.  Everything asynchronous on `st`.
+template <class MV>
+static hp_status run_lanczos(const hp_set_s* s, MV&& matvec, const double2* v0, int steps, bool reorth,
+                             LzState* state, double2* partial, double2* V, double2* w, cudaStream_t st) {
+  int64_t n = s->n;
+  int g = grid_for(n, 256, 148 * 16);
+  k_lz_init<<<1, 32, 0, st>>>(state, steps);
+  HP_LAUNCH_CHECK("k_lz_init");
+  hp_status rc = reduce(1, n, v0, nullptr, partial, state, 0, 1, 0.0, nullptr, st);
+  if (rc) return rc;
+  k_lz_div<<<g, 256, 0, st>>>(n, v0, V, state, 0, 0);
+  HP_LAUNCH_CHECK("k_lz_div");
+  for (int k = 0; k < steps; ++k) {
+    double2* vk = V + (int64_t)k * n;
+    rc = matvec(vk, w);
+    if (rc) return rc;
+    rc = reduce(0, n, vk, w, partial, state, k, 0, 0.0, nullptr, st);  // alpha_k
+    if (rc) return rc;
+    if (k == steps - 1) break;
+    k_lz_update<<<g, 256, 0, st>>>(n, w, vk, k > 0 ? V + (int64_t)(k - 1) * n : vk, state, k);
+    HP_LAUNCH_CHECK("k_lz_update");
+    if (reorth) {
+      for (int j = 0; j <= k; ++j) {
+        rc = reduce(0, n, V + (int64_t)j * n, w, partial, state, j, 3, 0.0, nullptr, st);
+        if (rc) return rc;
+      }
+      k_lz_reorth<<<g, 256, 0, st>>>(n, w, V, state, k);
+      HP_LAUNCH_CHECK("k_lz_reorth");
+    }
+    rc = reduce(1, n, w, nullptr, partial, state, k, 2, 1e-14, nullptr, st);  // beta_k
+    if (rc) return rc;
+    k_lz_div<<<g, 256, 0, st>>>(n, w, V + (int64_t)(k + 1) * n, state, k, 1);
+    HP_LAUNCH_CHECK("k_lz_div");
+  }
+  return HP_OK;
+}
+
+static hp_status check_m(int m) {
+  if (m < 1) return fail(HP_ERR_VALUE, "steps must be at least 1");
+  if (m > HP_MAXM) return fail(HP_ERR_VALUE, "krylov_steps exceeds the device limit of 48");
+  return HP_OK;
+}
+
+}  // namespace hp
+
+using namespace hp;
+
+extern "C" {
+
+size_t hp_reduce_workspace_bytes(int64_t n) {
+  (void)n;
+  return align_up(HP_RED_BLOCKS * sizeof(double2)) + align_up(sizeof(LzState));
+}
+
+hp_status hp_cdot(int64_t n, const void* a, const void* b, double* out, void* ws, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  return reduce(0, n, (const double2*)a, (const double2*)b, (double2*)ws, nullptr, 0, 4, 0.0, out, st);
+}
+
+hp_status hp_cnrm2(int64_t n, const void* a, double* out, void* ws, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  return reduce(1, n, (const double2*)a, nullptr, (double2*)ws, nullptr, 0, 5, 0.0, out, st);
+}
+
+hp_status hp_expm_tridiag_column(const double* alpha, const double* beta, int m, double tau, void* col,
+                                 int* status, void* stream) {
+  hp_status rc = check_m(m);
+  if (rc) return rc;
+  k_expm_standalone<<<1, 32, 0, as_stream(stream)>>>(alpha, beta, m, tau, (double2*)col, status);
+  HP_LAUNCH_CHECK("k_expm_standalone");
+  return HP_OK;
+}
+
+hp_status hp_tridiag_eigh(const double* alpha, const double* beta, int m, double* d, double* z, int* status,
+                          void* stream) {
+  hp_status rc = check_m(m);
+  if (rc) return rc;
+  k_tridiag_eigh<<<1, 32, 0, as_stream(stream)>>>(alpha, beta, m, d, z, status);
+  HP_LAUNCH_CHECK("k_tridiag_eigh");
+  return HP_OK;
+}
+
+size_t hp_magnus_workspace_bytes(hp_set_t s, int scheme, const int32_t* d1, int n1, const int32_t* d2, int n2,
+                                 int m) {
+  if (!s) return 0;
+  std::vector<double> ones(std::max(n1, n2) + 1, 1.0);
+  size_t pb = prog_bytes_for(s, make_terms(s->dim, d1, ones.data(), n1));
+  if (scheme == 1 && d2) pb = std::max(pb, prog_bytes_for(s, make_terms(s->dim, d2, ones.data(), n2)));
+  return lz_layout(s, m, scheme, pb).total;
+}
+
+hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* d1, const double* c1, int n1, const int32_t* d2,
+                         const double* c2, int n2, double halfwidth, double q, double h, int m, int reorth,
+                         void* y, double* diag, void* ws, size_t ws_bytes, void* stream) {
+  if (!s) return fail(HP_ERR_VALUE, "null set handle");
+  hp_status rc = check_m(m);
+  if (rc) return rc;
+  if (scheme != 0 && scheme != 1) return fail(HP_ERR_VALUE, "unknown scheme");
+  if (!(halfwidth > 0)) return fail(HP_ERR_VALUE, "halfwidth must be positive");
+  cudaStream_t st = as_stream(stream);
+  int64_t n = s->n;
+  Hamiltonian H1{s, {}, halfwidth, q, make_terms(s->dim, d1, c1, n1)};
+  H1.prog = build_program(s->dim, H1.terms, HP_ADD_OSC, nullptr);
+  Hamiltonian H2{s, {}, halfwidth, q, {}};
+  size_t pb = prog_bytes_for(s, H1.terms);
+  if (scheme == 1) {
+    H2.terms = make_terms(s->dim, d2, c2, n2);
+    H2.prog = build_program(s->dim, H2.terms, HP_ADD_OSC, nullptr);
+    pb = std::max(pb, prog_bytes_for(s, H2.terms));
+  }
+  LzLayout L = lz_layout(s, m, scheme, pb);
+  if (ws_bytes < L.total) return fail(HP_ERR_NOMEM, "workspace too small for hp_magnus_step");
+  char* base = (char*)ws;
+  LzState* state = (LzState*)(base + L.off_state);
+  double2* partial = (double2*)(base + L.off_partial);
+  double2* V = (double2*)(base + L.off_V);
+  double2* w = (double2*)(base + L.off_w);
+  double2* tmp = (double2*)(base + L.off_tmp);
+  double2* g = (double2*)(base + L.off_g);
+  double2* pws = (double2*)(base + L.off_prog);
+  size_t pws_bytes = L.total - L.off_prog;
+  double2* yv = (double2*)y;
+  double gamma = std::sqrt(3.0) / 12.0 * h;
+  auto mv = [&](const double2* v, double2* out) -> hp_status {
+    if (scheme == 0) return apply_ham_full(H1, v, out, tmp, pws, pws_bytes, st);
+    double2 *y1 = g, *y2 = g + n, *z2 = g + 2 * n, *z1 = g + 3 * n;
+    hp_status r;
+    if ((r = apply_ham_full(H1, v, y1, tmp, pws, pws_bytes, st))) return r;
+    if ((r = apply_ham_full(H2, v, y2, tmp, pws, pws_bytes, st))) return r;
+    if ((r = apply_ham_full(H2, y1, z2, tmp, pws, pws_bytes, st))) return r;
+    if ((r = apply_ham_full(H1, y2, z1, tmp, pws, pws_bytes, st))) return r;
+    k_gl2_combine<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, y1, y2, z2, z1, gamma, out);
+    HP_LAUNCH_CHECK("k_gl2_combine");
+    return HP_OK;
+  };
+  rc = run_lanczos(s, mv, yv, m, reorth != 0, state, partial, V, w, st);
+  if (rc) return rc;
+  k_lz_expm<<<1, 32, 0, st>>>(state, h);
+  HP_LAUNCH_CHECK("k_lz_expm");
+  k_lz_combine<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, V, state, yv);
+  HP_LAUNCH_CHECK("k_lz_combine");
+  if (diag) {
+    k_lz_diag<<<1, 32, 0, st>>>(state, diag, nullptr, nullptr);
+    HP_LAUNCH_CHECK("k_lz_diag");
+  }
+  return HP_OK;
+}
+
+hp_status hp_lanczos(hp_set_t s, const int32_t* d, const double* c, int nterms, double halfwidth, double q,
+                     const void* v0, int steps, int reorth, void* basis, double* alpha, double* beta, double* diag,
+                     void* ws, size_t ws_bytes, void* stream) {
+  if (!s) return fail(HP_ERR_VALUE, "null set handle");
+  hp_status rc = check_m(steps);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  Hamiltonian H{s, {}, halfwidth, q, make_terms(s->dim, d, c, nterms)};
+  H.prog = build_program(s->dim, H.terms, HP_ADD_OSC, nullptr);
+  LzLayout L = lz_layout(s, 0, 0, prog_bytes_for(s, H.terms));
+  if (ws_bytes < L.total) return fail(HP_ERR_NOMEM, "workspace too small for hp_lanczos");
+  char* base = (char*)ws;
+  LzState* state = (LzState*)(base + L.off_state);
+  double2* partial = (double2*)(base + L.off_partial);
+  double2* w = (double2*)(base + L.off_w);
+  double2* tmp = (double2*)(base + L.off_tmp);
+  double2* pws = (double2*)(base + L.off_prog);
+  size_t pws_bytes = L.total - L.off_prog;
+  auto mv = [&](const double2* v, double2* out) -> hp_status {
+    return apply_ham_full(H, v, out, tmp, pws, pws_bytes, st);
+  };
+  rc = run_lanczos(s, mv, (const double2*)v0, steps, reorth != 0, state, partial, (double2*)basis, w, st);
+  if (rc) return rc;
+  k_lz_diag<<<1, 32, 0, st>>>(state, diag, alpha, beta);
+  HP_LAUNCH_CHECK("k_lz_diag");
+  return HP_OK;
+}
+
+}  // extern "C"

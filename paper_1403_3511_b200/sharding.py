@@ -1,0 +1,119 @@
+"""Multi-GPU decomposition of full-cube states: slabs along j1.
+
+The vector of a full cube is C-ordered with j1 outermost, so the planes
+j1 in [lo, hi) of rank r are one contiguous block.  A polynomial whose
+largest axis-1 degree is r1 couples plane p only to planes p - r1 .. p + r1
+(every axis-1 factor is a Chebyshev sweep of at most r1 ladder steps), so
+each rank keeps a box [lo - h, hi + h) (h >= r1, clipped to the cube),
+receives the h boundary planes of each neighbour before every matvec, runs
+the local matvec on the box (a slab set: j1 keeps its global value, the
+faces of the box are treated as absent neighbours) and owns the exact
+result on [lo, hi).  The exchange is one contiguous send/recv pair per
+neighbour over NCCL (torch.distributed; gloo in the CPU tests).  Krylov
+inner products reduce per-rank partial sums in rank order (all_gather,
+then a fixed-order sum) so that every rank sees identical scalars.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+def partition(planes: int, world: int, rank: int) -> tuple[int, int]:
+    """Near-equal contiguous split of `planes` j1-planes over `world` ranks."""
+    base, extra = divmod(planes, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+@dataclass
+class SlabGeometry:
+    dim: int
+    bound: int
+    rank: int
+    world: int
+    halo: int
+
+    def __post_init__(self):
+        self.planes = self.bound + 1
+        self.plane = self.planes ** (self.dim - 1)
+        self.lo, self.hi = partition(self.planes, self.world, self.rank)
+        self.blo = max(0, self.lo - self.halo)
+        self.bhi = min(self.planes, self.hi + self.halo)
+        self.global_size = self.planes * self.plane
+
+    # element offsets inside the local box buffer
+    @property
+    def box_size(self) -> int:
+        return (self.bhi - self.blo) * self.plane
+
+    @property
+    def own_slice(self) -> slice:
+        return slice((self.lo - self.blo) * self.plane, (self.hi - self.blo) * self.plane)
+
+    def exchanges(self):
+        """(peer, send_slice, recv_slice) in box coordinates, lower neighbour first."""
+        out = []
+        p = self.plane
+        if self.rank > 0 and self.lo > self.blo:
+            depth = self.lo - self.blo
+            send = slice((self.lo - self.blo) * p, (self.lo - self.blo + depth) * p)
+            recv = slice(0, depth * p)
+            out.append((self.rank - 1, send, recv))
+        if self.rank < self.world - 1 and self.bhi > self.hi:
+            depth = self.bhi - self.hi
+            send = slice((self.hi - self.blo - depth) * p, (self.hi - self.blo) * p)
+            recv = slice((self.hi - self.blo) * p, (self.bhi - self.blo) * p)
+            out.append((self.rank + 1, send, recv))
+        return out
+
+
+def halo_exchange(geo: SlabGeometry, box, group=None) -> None:
+    """Fill the halo planes of `box` (a flat tensor of geo.box_size) from the neighbours."""
+    import torch.distributed as dist
+
+    ops = []
+    for peer, send, recv in geo.exchanges():
+        ops.append(dist.P2POp(dist.isend, box[send].contiguous() if not box[send].is_contiguous() else box[send],
+                              peer, group))
+        ops.append(dist.P2POp(dist.irecv, box[recv], peer, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+def fixed_order_sum(partial, group=None):
+    """Sum a per-rank tensor of partial sums in rank order (deterministic on every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    bufs = [torch.empty_like(partial) for _ in range(world)]
+    dist.all_gather(bufs, partial, group=group)
+    out = bufs[0].clone()
+    for b in bufs[1:]:
+        out += b
+    return out
+
+
+class SlabShard:
+    """One rank's slab of a full cube on the device (hp_set_create_slab)."""
+
+    def __init__(self, dim: int, bound: int, rank: int, world: int, halo: int):
+        from .index_set import build_slab
+
+        self.geo = SlabGeometry(dim, bound, rank, world, halo)
+        self.set = build_slab(dim, bound, self.geo.blo, self.geo.bhi)
+        self.global_size = self.geo.global_size
+
+    def local_coefficients(self, W, w):
+        """The box part (owned planes + halo) of the seeded global vector."""
+        c = W.coefficients(w)
+        g = self.geo
+        return c[g.blo * g.plane:g.bhi * g.plane].copy()
+
+    def apply_polynomial(self, appl, ap, x, y, flags: int = 0):
+        """y[own] = W(X) x on this rank's planes; x, y are box-sized device tensors."""
+        halo_exchange(self.geo, x)
+        appl.apply_into(ap, x, y, flags)

@@ -1,0 +1,124 @@
+"""Device Lanczos / Magnus propagation vs the reference (golden) and the oracle."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from oracle import hprop_oracle as O
+from paper_1403_3511_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def hp():
+    import paper_1403_3511_b200 as hp
+
+    return hp
+
+
+def test_tridiag_and_expm(hp, golden):
+    p = golden["propagate"]
+    d, z = hp.tridiag_eigh(p["tri_alpha"], p["tri_beta"])
+    assert rel_l2(d, p["tri_d"]) < 1e-14
+    # eigenvectors up to sign
+    for j in range(z.shape[1]):
+        s = np.sign(z[:, j] @ p["tri_z"][:, j])
+        assert rel_l2(s * z[:, j], p["tri_z"][:, j]) < 1e-13
+    col = hp.expm_tridiag_column(p["tri_alpha"], p["tri_beta"], 0.37)
+    assert rel_l2(col, p["tri_col"]) < 1e-14
+    d1, z1 = hp.tridiag_eigh(np.array([2.0]), np.array([]))
+    assert d1[0] == 2.0 and z1[0, 0] == 1.0
+
+
+def test_expm_against_scipy(hp):
+    from scipy.linalg import expm
+
+    rng = np.random.default_rng(3)
+    for m in (1, 2, 5, 12, 30):
+        a = rng.standard_normal(m)
+        b = np.abs(rng.standard_normal(m - 1)) + 0.1
+        T = np.diag(a) + np.diag(b, 1) + np.diag(b, -1)
+        col = hp.expm_tridiag_column(a, b, 0.7)
+        assert np.max(np.abs(col - expm(-0.7j * T)[:, 0])) < 1e-12
+
+
+def _fh(hp, w, s):
+    return hp.FastHamiltonian(s, hp.custom_potential(w.evaluator, w.dim, W.HALFWIDTH), w.degree)
+
+
+RUNS = [("cfg1", "cfg1", None, 100, 0.01, "midpoint"), ("cfg1gl2", "cfg1", None, 10, 0.01, "gl2"),
+        ("cfg3s", "cfg3", 255, 20, 0.001, "midpoint"), ("cfg4s", "cfg4", 15, 50, 0.005, "midpoint")]
+
+
+@pytest.mark.parametrize("name,base,bound,nsteps,dt,scheme", RUNS)
+def test_propagation_matches_reference(hp, golden, name, base, bound, nsteps, dt, scheme):
+    p = golden["propagate"]
+    w = W.CONFIGS[base] if bound is None else W.CONFIGS[base].scaled(bound, name)
+    s = hp.build_full(w.dim, w.bound) if w.kind == "full" else hp.build_hyperbolic(w.dim, w.bound)
+    c = W.coefficients(w, None if w.kind == "full" else s.indices)
+    fh = _fh(hp, w, s)
+    fac = hp.lanczos(fh.matvec_at(0.0), c, 7)
+    assert rel_l2(fac.alpha, p[f"{name}_lz_alpha"]) < 1e-13
+    assert rel_l2(fac.beta, p[f"{name}_lz_beta"]) < 1e-13
+    if w.kind == "full":  # reduced sets make W(X) non-normal: no orthogonality to pin
+        assert fac.orthogonality_defect() < 1e-10
+    y = hp.propagate_magnus(hp.MagnusScheme.from_name(scheme), fh.matvec_at, c, 0.0, nsteps * dt, nsteps, 7)
+    step = int(p[f"{name}_prop_step"])
+    assert rel_l2(y[::step], p[f"{name}_prop_samp"]) < TOL
+    assert np.linalg.norm(y) == pytest.approx(float(p[f"{name}_prop_norm"]), rel=TOL)
+    if f"{name}_prop_full" in p:
+        assert rel_l2(y, p[f"{name}_prop_full"]) < TOL
+
+
+def test_generic_matvec_lanczos_exactness(hp):
+    """Full-space Krylov exactness with a dense operator (krylov tests, :103-113)."""
+    from scipy.linalg import expm
+
+    rng = np.random.default_rng(5)
+    n = 6
+    A = rng.standard_normal((n, n))
+    A = A + A.T
+    v = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    y, fac = hp.lanczos_exp_apply(lambda x: A @ x, v, 0.3, n, reorthogonalize=True)
+    assert np.max(np.abs(y - expm(-0.3j * A) @ v)) < 1e-10
+
+
+def test_breakdown_truncates(hp):
+    s = hp.build_full(1, 9)
+    fh = hp.FastHamiltonian(s, hp.custom_potential(lambda p, t: 0.0 * p[:, 0], 1, 16.0), 2)
+    e = np.zeros(s.size, dtype=complex)
+    e[3] = 1.0  # an eigenvector of the oscillator diagonal: invariant subspace at once
+    fac = hp.lanczos(fh.matvec_at(0.0), e, 5)
+    assert fac.breakdown_at == 1 and fac.steps == 1
+    y = hp.propagate_magnus(hp.MagnusScheme.from_name("midpoint"), fh.matvec_at, e, 0.0, 0.5, 5, 5)
+    assert np.allclose(y[3], np.exp(-0.5j * 3.5), atol=1e-13)
+
+
+def test_norm_preserved_on_full_cube(hp):
+    w = W.CONFIGS["cfg4"].scaled(11, "cfg4x")
+    s = hp.build_full(w.dim, w.bound)
+    c = W.coefficients(w)
+    fh = _fh(hp, w, s)
+    y = hp.propagate_magnus(hp.MagnusScheme.from_name("midpoint"), fh.matvec_at, c, 0.0, 0.05, 10, 7)
+    assert abs(np.linalg.norm(y) - 1.0) < 1e-11
+
+
+def test_harmonic_part_route_vs_oracle(hp):
+    """harmonic_part != 0: exact square-sum route inside A(t)."""
+    s = hp.build_hyperbolic(3, 40)
+    spec = hp.torsional_minus_harmonic(3)
+    fh = hp.FastHamiltonian(s, spec, 6)
+    rng = np.random.default_rng(11)
+    c = rng.standard_normal(s.size) + 1j * rng.standard_normal(s.size)
+    c /= np.linalg.norm(c)
+    appl = O.applier_for_set(O.hyperbolic_indices(3, 40))
+    ham_at = O.hamiltonian_at(appl, spec.evaluator, 3, 16.0, 6, harmonic_part=spec.harmonic_part)
+    want = O.propagate("midpoint", ham_at, c, 0.0, 0.1, 5, 7)
+    got = hp.propagate_magnus(hp.MagnusScheme.from_name("midpoint"), fh.matvec_at, c, 0.0, 0.1, 5, 7)
+    assert rel_l2(got, want) < TOL
+    mv = fh.matvec_at(0.2)
+    ap = fh.approx_at(0.2)
+    want1 = appl.hamiltonian(ap.degrees, ap.coeffs, 16.0, c) + spec.harmonic_part * appl.square_sum(c)
+    assert rel_l2(mv(c), want1) < TOL

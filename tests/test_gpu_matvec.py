@@ -1,0 +1,314 @@
+"""GPU matvec parity: the sm_100a kernels vs the reference (golden) and the oracle.
+
+Tolerances (north_star): reference-order mode is bitwise identical to numpy;
+the default (regrouped / fused) evaluator is within relative L2 1e-12.
+"""
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+from oracle import hprop_oracle as O
+from paper_1403_3511_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def hp():
+    import paper_1403_3511_b200 as hp
+
+    return hp
+
+
+def _approx(degs, coeffs, dim, L=16.0, degree=None):
+    from paper_1403_3511_b200.potential_approx import ChebApprox
+
+    degs = np.asarray(degs)
+    return ChebApprox(dim, int(degree if degree is not None else (degs.max() if degs.size else 0)), L, 0.0,
+                      degs, np.asarray(coeffs), 0.0)
+
+
+# ---------------------------------------------------------------- dense oracle (reference test helpers)
+
+def dense_coordinate(iset, axis):
+    n = iset.size
+    mat = np.zeros((n, n))
+    for i, row in enumerate(iset.indices.tolist()):
+        k = row[axis - 1]
+        below = list(row)
+        below[axis - 1] = k - 1
+        if k > 0 and tuple(below) in iset:
+            mat[i, iset.position(tuple(below))] = math.sqrt(k / 2.0)
+        above = list(row)
+        above[axis - 1] = k + 1
+        if tuple(above) in iset:
+            mat[i, iset.position(tuple(above))] = math.sqrt((k + 1) / 2.0)
+    return mat
+
+
+def cheb_of_matrix(mat, deg):
+    t0 = np.eye(mat.shape[0])
+    if deg == 0:
+        return t0
+    t1 = mat
+    for _ in range(deg - 1):
+        t0, t1 = t1, 2.0 * mat @ t1 - t0
+    return t1
+
+
+def dense_surrogate(iset, approx):
+    xs = [dense_coordinate(iset, a) / approx.halfwidth for a in range(1, iset.dim + 1)]
+    out = np.zeros((iset.size, iset.size))
+    for row, alpha in approx.terms:
+        term = np.eye(iset.size)
+        for a in range(1, iset.dim + 1):
+            if row[a - 1] > 0:
+                term = term @ cheb_of_matrix(xs[a - 1], row[a - 1])
+        out += alpha * term
+    return out
+
+
+# ---------------------------------------------------------------- coordinate / chebyshev
+
+def test_coordinate_bitexact_golden(hp, golden):
+    m = golden["matvec"]
+    for key in [k for k in m if k.startswith("coord_") and k.endswith("_in")]:
+        _, dim, bound, axis, _ = key.split("_")
+        s = hp.build_hyperbolic(int(dim), int(bound))
+        got = hp.direct_op(s, int(axis), hp.CoeffVector(s, m[key])).data
+        assert np.array_equal(got, m[key.replace("_in", "_out")]), key
+
+
+@pytest.mark.parametrize("dim,bound,axis", [(1, 12, 1), (2, 10, 1), (2, 10, 2), (3, 6, 2)])
+def test_coordinate_matches_coupling_rule(hp, dim, bound, axis, rng):
+    s = hp.build_hyperbolic(dim, bound)
+    v = rng.standard_normal(s.size)
+    got = hp.direct_op(s, axis, hp.CoeffVector(s, v)).data
+    assert np.max(np.abs(got - dense_coordinate(s, axis) @ v)) < 1e-14
+
+
+def test_coordinate_respects_pruned_neighbors(hp):
+    s = hp.build_hyperbolic(2, 10)
+    e = np.zeros(s.size)
+    e[s.position((2, 2))] = 1.0
+    out = hp.direct_op(s, 1, hp.CoeffVector(s, e)).data
+    assert out[s.position((1, 2))] == pytest.approx(1.0)
+    assert np.count_nonzero(out) == 1
+
+
+def test_cheb_bitexact_golden(hp, golden):
+    m = golden["matvec"]
+    s = hp.build_hyperbolic(2, 12)
+    for deg in (0, 1, 2, 5, 8):
+        got = hp.cheb_of_coordinate_apply(s, 1, deg, 16.0, hp.CoeffVector(s, m["cheb_in"])).data
+        assert np.array_equal(got, m[f"cheb_{deg}_out"]), deg
+
+
+@pytest.mark.parametrize("deg", [0, 1, 2, 5, 8])
+def test_cheb_matches_matrix_recurrence(hp, deg, rng):
+    s = hp.build_hyperbolic(2, 12)
+    v = rng.standard_normal(s.size)
+    got = hp.cheb_of_coordinate_apply(s, 1, deg, 16.0, hp.CoeffVector(s, v)).data
+    want = cheb_of_matrix(dense_coordinate(s, 1) / 16.0, deg) @ v
+    assert np.max(np.abs(got - want)) < 1e-12
+
+
+# ---------------------------------------------------------------- whole surrogate
+
+def test_polynomial_golden(hp, golden):
+    m = golden["matvec"]
+    for key in [k for k in m if k.startswith("poly_") and k.endswith("_in")]:
+        base = key[:-3]
+        _, pot, dim, bound, degree = base.split("_")
+        s = hp.build_hyperbolic(int(dim), int(bound))
+        ap = _approx(m[base + "_degrees"], m[base + "_coeffs"], int(dim), degree=int(degree))
+        appl = hp.get_applier(s)
+        v = m[key]
+        # reference order: bitwise
+        assert np.array_equal(appl.apply_polynomial(ap, v, ref_order=True), m[base + "_out"]), base
+        assert np.array_equal(appl.apply_hamiltonian(ap, v, ref_order=True), m[base + "_ham"]), base
+        assert np.array_equal(appl.apply_square_sum(v), m[base + "_sq"]), base
+        order = list(range(1, int(dim) + 1))
+        assert np.array_equal(appl.apply_polynomial(ap, v, axis_order=order), m[base + "_order_fwd"])
+        # default (regrouped) evaluator: within tolerance
+        assert rel_l2(appl.apply_polynomial(ap, v), m[base + "_out"]) < TOL
+        assert rel_l2(appl.apply_hamiltonian(ap, v), m[base + "_ham"]) < TOL
+
+
+@pytest.mark.parametrize("dim,bound,degree,pot", [(1, 16, 7, "torsional"), (2, 12, 5, "torsional"),
+                                                  (2, 12, 5, "henon-heiles"), (3, 8, 3, "henon-heiles")])
+def test_matches_ordered_dense_product(hp, dim, bound, degree, pot, rng):
+    s = hp.build_hyperbolic(dim, bound)
+    ap = hp.interpolate(hp.smooth_remainder(hp.potential_by_name(pot, dim)), degree, time=0.4)
+    v = hp.CoeffVector(s, rng.standard_normal(s.size))
+    want = dense_surrogate(s, ap) @ v.data
+    scale = max(np.max(np.abs(want)), 1.0)
+    for ref in (False, True):
+        got = hp.fast_algorithm(s, ap, v, ref_order=ref).data
+        assert np.max(np.abs(got - want)) < 1e-13 * scale
+
+
+def test_grouped_equals_per_term(hp, rng):
+    for dim, bound in ((2, 30), (3, 12), (4, 10)):
+        s = hp.build_hyperbolic(dim, bound)
+        ap = hp.interpolate(hp.smooth_remainder(hp.henon_heiles_perturbed(dim)), 7, time=0.9)
+        appl = hp.get_applier(s)
+        v = rng.standard_normal(s.size)
+        ordered = appl.apply_polynomial(ap, v, axis_order=list(range(dim, 0, -1)))
+        for ref in (False, True):
+            grouped = appl.apply_polynomial(ap, v, ref_order=ref)
+            assert np.max(np.abs(grouped - ordered)) < 1e-14 * np.max(np.abs(ordered))
+
+
+def test_linearity(hp):
+    s = hp.build_hyperbolic(2, 10)
+    ap = hp.interpolate(hp.torsional(2), 4)
+    appl = hp.get_applier(s)
+    for seed in range(10):
+        gen = np.random.default_rng(seed)
+        a = gen.standard_normal(s.size) + 1j * gen.standard_normal(s.size)
+        b = gen.standard_normal(s.size)
+        sc = complex(gen.uniform(-8, 8), gen.uniform(-8, 8))
+        lhs = appl.apply_polynomial(ap, sc * a + b)
+        rhs = sc * appl.apply_polynomial(ap, a) + appl.apply_polynomial(ap, b)
+        assert np.max(np.abs(lhs - rhs)) < 1e-12 * max(np.max(np.abs(rhs)), 1.0)
+
+
+def test_axis_order_full_vs_pruned(hp, rng):
+    full = hp.build_full(2, 9)
+    ap = hp.interpolate(hp.smooth_remainder(hp.henon_heiles_perturbed(2)), 3, time=0.5)
+    v = hp.CoeffVector(full, rng.standard_normal(full.size))
+    a = hp.fast_algorithm(full, ap, v, axis_order=(2, 1))
+    b = hp.fast_algorithm(full, ap, v, axis_order=(1, 2))
+    assert np.max(np.abs(a.data - b.data)) < 1e-13
+    s = hp.build_hyperbolic(2, 12)
+    v = hp.CoeffVector(s, rng.standard_normal(s.size))
+    a = hp.fast_algorithm(s, ap, v, axis_order=(2, 1))
+    b = hp.fast_algorithm(s, ap, v, axis_order=(1, 2))
+    assert np.max(np.abs(a.data - b.data)) > 1e-9
+    with pytest.raises(ValueError, match="permute"):
+        hp.fast_algorithm(s, ap, v, axis_order=(1, 1))
+
+
+def test_errors_and_warnings(hp, rng):
+    s = hp.build_hyperbolic(2, 10)
+    other = hp.build_hyperbolic(2, 12)
+    ap = hp.interpolate(hp.torsional(2), 4)
+    with pytest.raises(ValueError, match="different index set"):
+        hp.fast_algorithm(s, ap, hp.CoeffVector(other, rng.standard_normal(other.size)))
+    v = hp.CoeffVector(s, rng.standard_normal(s.size))
+    with pytest.warns(UserWarning, match="exceeds half the basis bound"):
+        hp.fast_algorithm(s, hp.interpolate(hp.torsional(2), 8), v)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        hp.fast_algorithm(s, hp.interpolate(hp.torsional(2), 5), v)
+    f = hp.build_full(1, 6)
+    bad = hp.ChebApprox(dim=1, degree=1, halfwidth=1.0, time=0.0, degrees=np.array([[1]]),
+                        coeffs=np.array([1e308]), fit_error=0.0)
+    with pytest.raises(RuntimeError, match="non-finite"):
+        hp.fast_algorithm(f, bad, hp.CoeffVector(f, np.full(f.size, 1e3)))
+    with pytest.raises(ValueError):
+        hp.direct_op(s, 3, v)
+    assert hp.get_applier(s) is hp.get_applier(s)
+
+
+def test_hamiltonian_adds_oscillator_diagonal(hp, rng):
+    s = hp.build_hyperbolic(2, 10)
+    ap = hp.interpolate(hp.torsional(2), 4)
+    v = hp.CoeffVector(s, rng.standard_normal(s.size))
+    ham = hp.apply_hamiltonian(s, ap, v)
+    pot = hp.fast_algorithm(s, ap, v)
+    levels = (s.indices + 0.5).sum(axis=1)
+    assert np.max(np.abs(ham.data - pot.data - levels * v.data)) < 1e-14
+
+
+def test_batched_and_device_resident(hp, rng):
+    import torch
+
+    s = hp.build_hyperbolic(3, 20)
+    ap = hp.interpolate(hp.smooth_remainder(hp.henon_heiles_perturbed(3)), 4, time=0.2)
+    appl = hp.get_applier(s)
+    V = rng.standard_normal((5, s.size)) + 1j * rng.standard_normal((5, s.size))
+    Y = appl.apply_polynomial(ap, V)
+    for b in range(5):
+        assert np.array_equal(Y[b], appl.apply_polynomial(ap, V[b]))
+    Yd = appl.apply_polynomial(ap, torch.from_numpy(V).cuda())
+    assert Yd.is_cuda and np.array_equal(Yd.cpu().numpy(), Y)
+
+
+# ---------------------------------------------------------------- configuration workloads
+
+CASES = {"cfg1": ("cfg1", None), "cfg2": ("cfg2", None), "cfg3s": ("cfg3", 255), "cfg4s": ("cfg4", 15),
+         "cfg5s": ("cfg5", 63)}
+
+
+def _build(hp, w):
+    return hp.build_full(w.dim, w.bound) if w.kind == "full" else hp.build_hyperbolic(w.dim, w.bound)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_config_workloads_vs_golden(hp, golden, name):
+    m = golden["matvec"]
+    base, bound = CASES[name]
+    w = W.CONFIGS[base] if bound is None else W.CONFIGS[base].scaled(bound, name)
+    s = _build(hp, w)
+    c = W.coefficients(w, None if w.kind == "full" else s.indices)
+    vecs = c if c.ndim == 2 else c[None]
+    tt = 0.3 if "cfg4" in name else 0.0
+    t = golden["terms"]
+    ap = _approx(t[f"{base}_t{tt}_degrees"], t[f"{base}_t{tt}_coeffs"], w.dim, degree=w.degree)
+    appl = hp.get_applier(s)
+    step = int(m[f"{name}_in_step"])
+    assert np.array_equal(vecs[0][::step], m[f"{name}_in_samp"]), "seeded input differs from the golden run"
+    nb = min(vecs.shape[0], 4)
+    Y = appl.apply_polynomial(ap, vecs[:nb] if nb > 1 else vecs[0])
+    Y = Y.reshape(nb, -1)
+    Yr = appl.apply_polynomial(ap, vecs[:nb] if nb > 1 else vecs[0], ref_order=True).reshape(nb, -1)
+    for i in range(nb):
+        samp = m[f"{name}_poly{i}_samp"]
+        assert np.array_equal(Yr[i][::step], samp), (name, i)
+        assert rel_l2(Y[i][::step], samp) < TOL, (name, i)
+        assert np.linalg.norm(Y[i]) == pytest.approx(float(m[f"{name}_poly{i}_norm"]), rel=TOL)
+    H = appl.apply_hamiltonian(ap, vecs[0])
+    assert rel_l2(H[::step], m[f"{name}_ham_samp"]) < TOL
+    if f"{name}_poly0_full" in m:
+        assert rel_l2(Y[0], m[f"{name}_poly0_full"]) < TOL
+        assert np.array_equal(Yr[0], m[f"{name}_poly0_full"])
+
+
+def test_cfg2_full_vs_oracle(hp):
+    w = W.CONFIGS["cfg2"]
+    s = hp.build_full(w.dim, w.bound)
+    c = W.coefficients(w)
+    ap = w.approx()
+    want = O.applier_for_full(w.dim, w.bound).polynomial(ap.degrees, ap.coeffs, 16.0, c)
+    got = hp.get_applier(s).apply_polynomial(ap, c)
+    assert rel_l2(got, want) < TOL
+    assert np.array_equal(hp.get_applier(s).apply_polynomial(ap, c, ref_order=True), want)
+
+
+@pytest.mark.slow
+def test_cfg4_full_size_slab_vs_oracle(hp):
+    """Full-size cfg4 (2.7e8 coefficients): GPU output on planes j1 in [62, 64) equals the oracle
+    evaluated on the slab box [58, 68) (its r1 = 4 halo makes those planes exact)."""
+    import torch
+
+    w = W.CONFIGS["cfg4"]
+    s = hp.build_full(w.dim, w.bound)
+    c = W.coefficients(w)
+    ap = w.approx(0.3)
+    y = hp.get_applier(s).apply_polynomial(ap, torch.from_numpy(c).cuda())
+    plane = (w.bound + 1) ** 3
+    lo, hi, blo, bhi = 62, 64, 58, 68
+    slab = O.applier_for_slab(w.dim, w.bound, blo, bhi)
+    want = slab.polynomial(ap.degrees, ap.coeffs, 16.0, c[blo * plane:bhi * plane])
+    got = y[lo * plane:hi * plane].cpu().numpy()
+    assert rel_l2(got, want[(lo - blo) * plane:(hi - blo) * plane]) < TOL
+    # linearity at full size
+    y2 = hp.get_applier(s).apply_polynomial(ap, 2.0 * torch.from_numpy(c).cuda())
+    assert float(torch.linalg.vector_norm(y2 - 2.0 * y) / torch.linalg.vector_norm(y)) < 1e-14
