@@ -156,6 +156,9 @@ struct AllTab {
 
 static int g_blocks(int64_t n) { return grid_for(n, 256, 148 * 16); }
 
+// workspace cap per call of the generic program; batches beyond it are chunked
+static const size_t kChunkCap = (size_t)24 << 30;
+
 template <class T>
 static hp_status launch_cheb(const hp_set_s* s, int a, int mode, double scale, const T* w, const T* wm,
                              T* out, T* acc, double hw, int64_t batch, cudaStream_t st) {
@@ -528,7 +531,10 @@ size_t hp_poly_workspace_bytes(hp_set_t s, const int32_t* degrees, int nterms, i
   Program p = build_program(s->dim, terms, flags, nullptr);
   int ns = std::max(p.nslots, 4);
   size_t fg = fullgrid_workspace_bytes(s, terms, dtype, batch, flags);
-  size_t gen = (size_t)ns * s->n * batch * (dtype == HP_C128 ? 16 : 8);
+  size_t per_vec = (size_t)ns * s->n * (dtype == HP_C128 ? 16 : 8);
+  // large batches run in chunks whose trie workspace stays below kChunkCap
+  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(kChunkCap / std::max<size_t>(per_vec, 1))));
+  size_t gen = per_vec * chunk;
   return std::max(gen, fg);
 }
 
@@ -555,11 +561,21 @@ hp_status hp_apply_polynomial(hp_set_t s, const int32_t* degrees, const double* 
   }
   if (!done) {
     Program p = build_program(s->dim, terms, flags, axis_order);
-    if (dtype == HP_C128)
-      rc = run_program<double2>(s, p, halfwidth, (const double2*)in, (double2*)out, batch, (double2*)ws, ws_bytes, st);
-    else
-      rc = run_program<double>(s, p, halfwidth, (const double*)in, (double*)out, batch, (double*)ws, ws_bytes, st);
-    if (rc) return rc;
+    size_t es = dtype == HP_C128 ? 16 : 8;
+    size_t per_vec = (size_t)std::max(p.nslots, 1) * s->n * es;
+    int64_t chunk = std::min<int64_t>(batch, (int64_t)(ws_bytes / per_vec));
+    if (chunk < 1) return fail(HP_ERR_NOMEM, "workspace too small for the polynomial program");
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+      int64_t nb = std::min(chunk, batch - b0);
+      size_t off = (size_t)b0 * s->n * es;
+      if (dtype == HP_C128)
+        rc = run_program<double2>(s, p, halfwidth, (const double2*)((const char*)in + off),
+                                  (double2*)((char*)out + off), nb, (double2*)ws, ws_bytes, st);
+      else
+        rc = run_program<double>(s, p, halfwidth, (const double*)((const char*)in + off), (double*)((char*)out + off),
+                                 nb, (double*)ws, ws_bytes, st);
+      if (rc) return rc;
+    }
   }
   if (flags & HP_CHECK_FINITE) {
     bool ok = true;

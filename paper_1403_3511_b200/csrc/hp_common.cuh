@@ -9,6 +9,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -121,6 +122,11 @@ struct hp_set_s {
   int64_t* d_off = nullptr;
   // custom sets keep a host copy of the indices for position()
   std::vector<int64_t> h_indices;
+  // full cubes: banded basis tables T_k(X_l / L) per axis, built on first use
+  // of the fused evaluator (hp_fullgrid.cu) and cached per halfwidth
+  mutable std::mutex fg_mtx;
+  mutable double fg_L = 0.0;
+  mutable double* fg_basis = nullptr;
 
   hp::AxBox box(int a) const {
     hp::AxBox v;

@@ -39,6 +39,9 @@ class SlabGeometry:
         self.planes = self.bound + 1
         self.plane = self.planes ** (self.dim - 1)
         self.lo, self.hi = partition(self.planes, self.world, self.rank)
+        if self.planes // self.world < self.halo and self.world > 1:
+            raise ValueError(f"{self.planes} planes over {self.world} ranks leave fewer owned planes "
+                             f"than the halo depth {self.halo}")
         self.blo = max(0, self.lo - self.halo)
         self.bhi = min(self.planes, self.hi + self.halo)
         self.global_size = self.planes * self.plane
@@ -53,17 +56,21 @@ class SlabGeometry:
         return slice((self.lo - self.blo) * self.plane, (self.hi - self.blo) * self.plane)
 
     def exchanges(self):
-        """(peer, send_slice, recv_slice) in box coordinates, lower neighbour first."""
+        """(peer, send_slice, recv_slice) in box coordinates, lower neighbour first.
+
+        What is sent is sized by the *peer's* halo (its box may be clipped
+        differently at the cube faces); what is received by our own.
+        """
         out = []
         p = self.plane
-        if self.rank > 0 and self.lo > self.blo:
-            depth = self.lo - self.blo
-            send = slice((self.lo - self.blo) * p, (self.lo - self.blo + depth) * p)
-            recv = slice(0, depth * p)
+        if self.rank > 0:
+            send_depth = min(self.halo, self.planes - self.lo)   # upper halo of rank - 1
+            send = slice((self.lo - self.blo) * p, (self.lo - self.blo + send_depth) * p)
+            recv = slice(0, (self.lo - self.blo) * p)
             out.append((self.rank - 1, send, recv))
-        if self.rank < self.world - 1 and self.bhi > self.hi:
-            depth = self.bhi - self.hi
-            send = slice((self.hi - self.blo - depth) * p, (self.hi - self.blo) * p)
+        if self.rank < self.world - 1:
+            send_depth = min(self.halo, self.hi)                 # lower halo of rank + 1
+            send = slice((self.hi - self.blo - send_depth) * p, (self.hi - self.blo) * p)
             recv = slice((self.hi - self.blo) * p, (self.bhi - self.blo) * p)
             out.append((self.rank + 1, send, recv))
         return out
@@ -73,11 +80,13 @@ def halo_exchange(geo: SlabGeometry, box, group=None) -> None:
     """Fill the halo planes of `box` (a flat tensor of geo.box_size) from the neighbours."""
     import torch.distributed as dist
 
+    import torch
+
+    buf = torch.view_as_real(box) if box.is_complex() else box  # plane slices stay contiguous
     ops = []
     for peer, send, recv in geo.exchanges():
-        ops.append(dist.P2POp(dist.isend, box[send].contiguous() if not box[send].is_contiguous() else box[send],
-                              peer, group))
-        ops.append(dist.P2POp(dist.irecv, box[recv], peer, group))
+        ops.append(dist.P2POp(dist.isend, buf[send], peer, group))
+        ops.append(dist.P2POp(dist.irecv, buf[recv], peer, group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()

@@ -292,6 +292,26 @@ def test_cfg2_full_vs_oracle(hp):
     assert np.array_equal(hp.get_applier(s).apply_polynomial(ap, c, ref_order=True), want)
 
 
+@pytest.mark.parametrize("bound", [3, 5, 11, 20])
+def test_fused_fullgrid_sizes_and_slabs(hp, bound):
+    """The fused two-pass N=4 evaluator (hp_fullgrid.cu) at ragged sizes, on cubes and j1-slabs."""
+    w = W.CONFIGS["cfg4"].scaled(bound, "cfg4x")
+    ap = w.approx(0.3)
+    c = W.coefficients(w)
+    oa = O.applier_for_full(w.dim, w.bound)
+    s = hp.build_full(w.dim, w.bound)
+    appl = hp.get_applier(s)
+    assert rel_l2(appl.apply_polynomial(ap, c), oa.polynomial(ap.degrees, ap.coeffs, 16.0, c)) < TOL
+    assert rel_l2(appl.apply_hamiltonian(ap, c), oa.hamiltonian(ap.degrees, ap.coeffs, 16.0, c)) < TOL
+    side = w.bound + 1
+    plane = side ** 3
+    for lo, hi in [(0, side // 2), (side // 3, side), (1, max(2, side - 1))]:
+        sl = hp.build_slab(w.dim, w.bound, lo, hi)
+        ob = O.applier_for_slab(w.dim, w.bound, lo, hi)
+        x = c[lo * plane:hi * plane]
+        assert rel_l2(hp.get_applier(sl).apply_hamiltonian(ap, x), ob.hamiltonian(ap.degrees, ap.coeffs, 16.0, x)) < TOL
+
+
 @pytest.mark.slow
 def test_cfg4_full_size_slab_vs_oracle(hp):
     """Full-size cfg4 (2.7e8 coefficients): GPU output on planes j1 in [62, 64) equals the oracle
