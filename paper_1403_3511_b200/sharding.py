@@ -92,6 +92,17 @@ def halo_exchange(geo: SlabGeometry, box, group=None) -> None:
             req.wait()
 
 
+def emulate_exchange(geos, boxes) -> None:
+    """Single-process stand-in for halo_exchange over all ranks (tests): the same
+    plan, executed as device-to-device copies between the ranks' boxes."""
+    for g, box in zip(geos, boxes):
+        for peer, _send, recv in g.exchanges():
+            pg = geos[peer]
+            # the peer's matching send slice is the one addressed to us
+            psend = [s for p, s, _ in pg.exchanges() if p == g.rank][0]
+            box[recv] = boxes[peer][psend]
+
+
 def fixed_order_sum(partial, group=None):
     """Sum a per-rank tensor of partial sums in rank order (deterministic on every rank)."""
     import torch
