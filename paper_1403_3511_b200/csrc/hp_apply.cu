@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <map>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "hp_common.cuh"
@@ -94,6 +95,23 @@ __global__ void k_osc(int64_t n, int64_t batch, int dim, AXS axs, const T* __res
     for (int a = 0; a < dim; ++a) lev += (double)axs.j(a, o) + 0.5;
     for (int64_t b = 0; b < batch; ++b) acc[b * n + o] = sadd(acc[b * n + o], smul(lev, ldg(v + b * n + o)));
   }
+}
+
+// acc += levels * v, and one partial of <v, acc_new> per CTA (Lanczos alpha, fused)
+template <class AXS>
+__global__ void k_osc_dot(int64_t n, int dim, AXS axs, const double2* __restrict__ v, double2* __restrict__ acc,
+                          double2* __restrict__ partial) {
+  double2 d = make_double2(0.0, 0.0);
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+    double lev = 0.0;
+    for (int a = 0; a < dim; ++a) lev += (double)axs.j(a, o) + 0.5;
+    double2 x = ldg(v + o);
+    double2 y = sadd(acc[o], smul(lev, x));
+    acc[o] = y;
+    cdot_acc(x, y, d);
+  }
+  d = block_sum2(d);
+  if (threadIdx.x == 0) partial[blockIdx.x] = d;
 }
 
 template <class T>
@@ -366,8 +384,29 @@ Program build_program(int dim, const std::vector<Term>& terms, int flags, const 
 }
 
 template <class T>
+static hp_status launch_osc_dot(const hp_set_s* s, const T* v, T* acc, DotOut* dot, cudaStream_t st) {
+  if constexpr (std::is_same<T, double2>::value) {
+    int64_t n = s->n;
+    int g = std::min(g_blocks(n), dot->capacity);
+    if (s->boxed) {
+      AllBox ab;
+      for (int a = 0; a < s->dim; ++a) ab.ax[a] = s->box(a);
+      k_osc_dot<AllBox><<<g, 256, 0, st>>>(n, s->dim, ab, v, acc, dot->partial);
+    } else {
+      AllTab at;
+      for (int a = 0; a < s->dim; ++a) at.ax[a] = s->tab(a);
+      k_osc_dot<AllTab><<<g, 256, 0, st>>>(n, s->dim, at, v, acc, dot->partial);
+    }
+    HP_LAUNCH_CHECK("k_osc_dot");
+    dot->n = g;
+  }
+  return HP_OK;
+}
+
+template <class T>
 hp_status run_program(const hp_set_s* s, const Program& p, double halfwidth, const T* v, T* y,
-                      int64_t batch, T* ws, size_t ws_bytes, cudaStream_t st) {
+                      int64_t batch, T* ws, size_t ws_bytes, cudaStream_t st, DotOut* dot) {
+  if (dot) dot->n = 0;
   int64_t n = s->n;
   int64_t vec = n * batch;
   if ((size_t)p.nslots * vec * sizeof(T) > ws_bytes)
@@ -402,7 +441,11 @@ hp_status run_program(const hp_set_s* s, const Program& p, double halfwidth, con
                             op.acc != -100 ? buf(op.acc) : nullptr, op.hw, batch, st);
         break;
       case OP_OSC:
-        rc = launch_osc<T>(s, buf(op.a), buf(op.dst), batch, st);
+        if (dot && dot->partial && batch == 1 && op.dst == BUF_Y && op.a == BUF_V && &op == &p.ops.back() &&
+            std::is_same<T, double2>::value)
+          rc = launch_osc_dot<T>(s, buf(op.a), buf(op.dst), dot, st);
+        else
+          rc = launch_osc<T>(s, buf(op.a), buf(op.dst), batch, st);
         break;
     }
     if (rc != HP_OK) return rc;
@@ -410,9 +453,9 @@ hp_status run_program(const hp_set_s* s, const Program& p, double halfwidth, con
   return HP_OK;
 }
 template hp_status run_program<double>(const hp_set_s*, const Program&, double, const double*, double*,
-                                       int64_t, double*, size_t, cudaStream_t);
+                                       int64_t, double*, size_t, cudaStream_t, DotOut*);
 template hp_status run_program<double2>(const hp_set_s*, const Program&, double, const double2*, double2*,
-                                        int64_t, double2*, size_t, cudaStream_t);
+                                        int64_t, double2*, size_t, cudaStream_t, DotOut*);
 
 template <class T>
 hp_status check_finite(const T* y, int64_t total, cudaStream_t st, bool* ok) {

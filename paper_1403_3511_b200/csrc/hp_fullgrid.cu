@@ -219,16 +219,20 @@ static hp_status launch_inner(const hp_set_s* s, const double2* v, double2* u, c
 
 template <int RM, int NMIX, unsigned M0, unsigned M1>
 static hp_status launch_outer(const hp_set_s* s, const double2* v, const double2* u, double2* y, const double* P,
-                              const double* G, const FgPlan& F, cudaStream_t st) {
+                              const double* G, const FgPlan& F, cudaStream_t st, DotOut* dot) {
   int n0 = s->side[0], n1 = s->side[1];
   int tile = n1 * FG_C;
+  const int64_t nblk = (int64_t)s->side[2] * s->side[3] / FG_C;
+  const bool use_dot = dot && dot->partial && nblk <= dot->capacity;
   size_t smem = ((size_t)FGA_NS * (n1 + 2 * FG_K) * FG_C + (size_t)FGA_NU * tile) * sizeof(double2);
   auto kern = k_fg_outer2<RM, NMIX, M0, M1>;
   HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int threads = (tile + 31) / 32 * 32;
   int64_t inner = (int64_t)s->side[2] * s->side[3];
   kern<<<(unsigned)(inner / FG_C), threads, smem, st>>>(v, u, y, P, P + FG_MAXN * FG_W, G, s->fg_basis, n0, n1,
-                                                       s->stride[0], s->stride[1], F.r0[0], F.r0[1]);
+                                                       s->stride[0], s->stride[1], F.r0[0], F.r0[1],
+                                                       use_dot ? dot->partial : nullptr);
+  if (use_dot) dot->n = (int)(inner / FG_C);
   HP_LAUNCH_CHECK("k_fg_outer2");
   return HP_OK;
 }
@@ -242,7 +246,8 @@ size_t fullgrid_workspace_bytes(const hp_set_s* s, const std::vector<Term>& term
 
 hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                          const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
-                         cudaStream_t st, bool* done) {
+                         cudaStream_t st, bool* done, DotOut* dot) {
+  if (dot) dot->n = 0;
   *done = false;
   FgPlan F = classify(s, terms, dtype, batch, flags);
   if (!F.ok) return HP_OK;
@@ -275,17 +280,17 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   if (rc) return rc;
   // pass A
   if (F.nmix == 0 && even && F.mask[1] == FG_MASK_EVEN)
-    rc = launch_outer<0, 0, FG_MASK_EVEN, FG_MASK_EVEN>(s, v, u, y, P, G, F, st);
+    rc = launch_outer<0, 0, FG_MASK_EVEN, FG_MASK_EVEN>(s, v, u, y, P, G, F, st, dot);
   else if (F.nmix == 1 && F.rm == 1 && even && F.mask[1] == FG_MASK_EVEN_PM1)
-    rc = launch_outer<1, 1, FG_MASK_EVEN, FG_MASK_EVEN_PM1>(s, v, u, y, P, G, F, st);
+    rc = launch_outer<1, 1, FG_MASK_EVEN, FG_MASK_EVEN_PM1>(s, v, u, y, P, G, F, st, dot);
   else if (F.nmix == 0)
-    rc = launch_outer<0, 0, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st);
+    rc = launch_outer<0, 0, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st, dot);
   else if (F.nmix == 1 && F.rm == 1)
-    rc = launch_outer<1, 1, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st);
+    rc = launch_outer<1, 1, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st, dot);
   else if (F.nmix == 1)
-    rc = launch_outer<2, 1, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st);
+    rc = launch_outer<2, 1, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st, dot);
   else
-    rc = launch_outer<2, 2, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st);
+    rc = launch_outer<2, 2, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st, dot);
   if (rc) return rc;
   *done = true;
   return HP_OK;

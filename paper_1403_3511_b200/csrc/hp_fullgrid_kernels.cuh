@@ -137,8 +137,9 @@ __global__ void __launch_bounds__(512, 1) k_fg_outer2(const double2* __restrict_
                                                       double2* __restrict__ y, const double* __restrict__ P0,
                                                       const double* __restrict__ P1, const double* __restrict__ G,
                                                       const double* __restrict__ B0, int n0, int n1, int64_t S0,
-                                                      int64_t S1, int r0a, int r0b) {
+                                                      int64_t S1, int r0a, int r0b, double2* __restrict__ dotp) {
   constexpr int WS = RM + 1, WG = 2 * RM + 1;
+  double2 dacc = zz();  // <v, y> partial (Lanczos alpha), only if dotp
   constexpr int U = clcm(FG_W, clcm(WS, WG));
   constexpr int NM = NMIX > 0 ? NMIX : 1;
   extern __shared__ double2 sm[];
@@ -267,10 +268,16 @@ __global__ void __launch_bounds__(512, 1) k_fg_outer2(const double2* __restrict_
 #pragma unroll
         for (int d = -RM; d <= RM; ++d) fma2(tb[m][d + RM], GW[m][(k + d + RM) % WG], acc);
       }
-      y[(int64_t)p * S0 + off] = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+      const double2 out = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+      y[(int64_t)p * S0 + off] = out;
+      if (dotp) cdot_acc(V[(k + FG_K) % FG_W], out, dacc);
     });
   }
   cp_wait<0>();
+  if (dotp) {
+    dacc = block_sum2(dacc);
+    if (t == 0) dotp[blockIdx.x] = dacc;
+  }
 }
 
 }  // namespace hp

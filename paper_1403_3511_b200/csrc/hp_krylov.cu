@@ -22,9 +22,13 @@
 
 namespace hp {
 
+// Scaled Lanczos: the basis is stored unnormalised (row k holds w_k with
+// v_k = scale[k] * w_k), so no separate normalisation pass is needed; the
+// scales enter the next update and the final combine as scalars.
 struct LzState {
   double alpha[HP_MAXM];
   double beta[HP_MAXM];
+  double scale[HP_MAXM];
   double2 col[HP_MAXM];
   double2 reo[HP_MAXM];
   double nrm0;
@@ -90,8 +94,25 @@ __global__ void __launch_bounds__(HP_RED_THREADS) k_red_final(const double2* par
   if (what == 0) {
     st->alpha[k] = s.x;
     st->defect = fmax(st->defect, fabs(s.y));
+  } else if (what == 6) {  // alpha_k = s_k^2 <w_k, A w_k>
+    double s2 = st->scale[k] * st->scale[k];
+    st->alpha[k] = s2 * s.x;
+    st->defect = fmax(st->defect, fabs(s2 * s.y));
+  } else if (what == 7) {  // beta_k = ||w_{k+1}||, scale_{k+1} = 1 / beta_k
+    double bk = sqrt(s.x);
+    if (bk <= tol) {
+      st->broken = 1;
+      st->m_eff = k + 1;
+      st->breakdown_at = k + 1;
+    } else {
+      st->beta[k] = bk;
+      st->scale[k + 1] = 1.0 / bk;
+    }
+  } else if (what == 8) {  // reorthogonalisation coefficient c_k = s_k <w_k, w'>
+    st->reo[k] = make_double2(st->scale[k] * s.x, st->scale[k] * s.y);
   } else if (what == 1) {
     st->nrm0 = sqrt(s.x);
+    st->scale[0] = 1.0 / st->nrm0;
   } else if (what == 2) {
     double bk = sqrt(s.x);
     st->scratch = bk;
@@ -183,6 +204,87 @@ __global__ void k_lz_combine(int64_t n, const double2* __restrict__ V, const LzS
       acc.y += v.x * c.y + v.y * c.x;
     }
     y[i] = make_double2(s * acc.x, s * acc.y);
+  }
+}
+
+// scaled update w_{k+1} = s_k z - alpha_k s_k w_k - beta_{k-1} s_{k-1} w_{k-1}
+// (= A v_k - alpha_k v_k - beta_{k-1} v_{k-1}, krylov_propagator.py:86) fused with
+// the partial sums of ||w_{k+1}||^2 (:89)
+__global__ void __launch_bounds__(HP_RED_THREADS) k_lz_update_s(int64_t n, const double2* __restrict__ z,
+                                                                const double2* __restrict__ wk,
+                                                                const double2* __restrict__ wkm1,
+                                                                double2* __restrict__ wn, const LzState* st, int k,
+                                                                double2* __restrict__ partial) {
+  __shared__ double2 sh[HP_RED_THREADS];
+  double2 acc = make_double2(0.0, 0.0);
+  if (!(st->broken && k >= st->m_eff)) {
+    const double sk = st->scale[k];
+    const double ca = st->alpha[k] * sk;
+    const double cb = k > 0 ? st->beta[k - 1] * st->scale[k - 1] : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      double2 a = __ldg(z + i), b = __ldg(wk + i);
+      double2 r = make_double2(fma(sk, a.x, -ca * b.x), fma(sk, a.y, -ca * b.y));
+      if (k > 0) {
+        double2 c = __ldg(wkm1 + i);
+        r.x = fma(-cb, c.x, r.x);
+        r.y = fma(-cb, c.y, r.y);
+      }
+      wn[i] = r;
+      acc.x = fma(r.x, r.x, fma(r.y, r.y, acc.x));
+    }
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = HP_RED_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = cadd(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+// scaled reorthogonalisation: w' -= sum_{j<=k} reo[j] s_j w_j  (reo[j] = <v_j, w'>)
+__global__ void k_lz_reorth_s(int64_t n, double2* __restrict__ w, const double2* __restrict__ w0,
+                              const double2* __restrict__ V, const LzState* st, int k) {
+  if (st->broken && k >= st->m_eff) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = 0; j <= k; ++j) {
+      double2 c = st->reo[j];
+      double sj = st->scale[j];
+      double2 v = __ldg((j == 0 ? w0 : V + (int64_t)(j - 1) * n) + i);
+      acc.x += sj * (c.x * v.x - c.y * v.y);
+      acc.y += sj * (c.x * v.y + c.y * v.x);
+    }
+    w[i] = ssub(w[i], acc);
+  }
+}
+
+// y = nrm0 * sum_{k < m_eff} col_k s_k w_k  (krylov_propagator.py:186); row 0 may alias y
+__global__ void k_lz_combine_s(int64_t n, const double2* w0, const double2* __restrict__ V, const LzState* st,
+                               double2* y) {
+  const int m = st->m_eff;
+  const double s = st->nrm0;
+  double2 c[HP_MAXM];
+  for (int k = 0; k < m; ++k) c[k] = make_double2(st->col[k].x * st->scale[k], st->col[k].y * st->scale[k]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < m; ++k) {
+      double2 v = (k == 0 ? w0 : V + (int64_t)(k - 1) * n)[i];
+      acc.x += v.x * c[k].x - v.y * c[k].y;
+      acc.y += v.x * c[k].y + v.y * c[k].x;
+    }
+    y[i] = make_double2(s * acc.x, s * acc.y);
+  }
+}
+
+// rows k >= 1 of an unnormalised basis -> v_k = s_k w_k (hp_lanczos output)
+__global__ void k_lz_normalize_rows(int64_t n, double2* __restrict__ B, const LzState* st) {
+  const int m = st->m_eff;
+  for (int k = 0; k < m; ++k) {
+    const double s = st->scale[k];
+    double2* row = B + (int64_t)k * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      row[i] = make_double2(row[i].x * s, row[i].y * s);
   }
 }
 
@@ -352,11 +454,12 @@ struct Hamiltonian {
 };
 
 static hp_status apply_ham(const Hamiltonian& H, const double2* v, double2* y, double2* ws, size_t ws_bytes,
-                           cudaStream_t st) {
+                           cudaStream_t st, DotOut* dot) {
   bool done = false;
-  hp_status rc = fullgrid_apply(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done);
+  hp_status rc = fullgrid_apply(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done,
+                                dot);
   if (rc) return rc;
-  if (!done) rc = run_program<double2>(H.s, H.prog, H.halfwidth, v, y, 1, ws, ws_bytes, st);
+  if (!done) rc = run_program<double2>(H.s, H.prog, H.halfwidth, v, y, 1, ws, ws_bytes, st, dot);
   return rc;
 }
 
@@ -365,10 +468,12 @@ __global__ void k_axpy_c2(int64_t n, double c, const double2* __restrict__ x, do
     acc[i] = sadd(acc[i], smul(c, __ldg(x + i)));
 }
 
+// A(t) v; if `dot` is given and the evaluator could fuse it, dot->n partials of <v, A v>
 static hp_status apply_ham_full(const Hamiltonian& H, const double2* v, double2* y, double2* tmp, double2* ws,
-                                size_t ws_bytes, cudaStream_t st) {
-  hp_status rc = apply_ham(H, v, y, ws, ws_bytes, st);
+                                size_t ws_bytes, cudaStream_t st, DotOut* dot = nullptr) {
+  hp_status rc = apply_ham(H, v, y, ws, ws_bytes, st, H.q == 0.0 ? dot : nullptr);
   if (rc) return rc;
+  if (dot && H.q != 0.0) dot->n = 0;
   if (H.q != 0.0) {
     rc = launch_square<double2>(H.s, v, tmp, 1, st);
     if (rc) return rc;
@@ -382,18 +487,20 @@ static hp_status apply_ham_full(const Hamiltonian& H, const double2* v, double2*
 // ---------------------------------------------------------------- workspace layout
 
 struct LzLayout {
-  size_t off_state, off_partial, off_V, off_w, off_tmp, off_g, off_prog, total;
+  size_t off_state, off_partial, off_dot, off_V, off_w, off_tmp, off_g, off_prog, total;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static LzLayout lz_layout(const hp_set_s* s, int m, int scheme, size_t prog_bytes) {
+// `rows`: basis rows kept in the workspace (row 0 is the caller's vector)
+static LzLayout lz_layout(const hp_set_s* s, int rows, int scheme, size_t prog_bytes) {
   LzLayout L;
   size_t vec = (size_t)s->n * 16;
   size_t o = 0;
   L.off_state = o; o = align_up(o + sizeof(LzState));
   L.off_partial = o; o = align_up(o + HP_RED_BLOCKS * sizeof(double2));
-  L.off_V = o; o = align_up(o + (size_t)m * vec);
+  L.off_dot = o; o = align_up(o + HP_DOT_CAPACITY * sizeof(double2));
+  L.off_V = o; o = align_up(o + (size_t)std::max(rows, 0) * vec);
   L.off_w = o; o = align_up(o + vec);
   L.off_tmp = o; o = align_up(o + vec);
   L.off_g = o; o = align_up(o + (scheme == 1 ? 4 * vec : 0));
@@ -409,40 +516,54 @@ static size_t prog_bytes_for(const hp_set_s* s, const std::vector<Term>& terms) 
   return std::max(gen, fg);
 }
 
-// Run the Lanczos recurrence for `steps` iterations with matvec = op.
-// V: steps x n rows.  Everything asynchronous on `st`.
+// Scaled Lanczos recurrence (krylov_propagator.py:58-104) for `steps`
+// iterations.  w0 = starting vector (row 0, read only); rows 1..steps-1 are
+// written unnormalised into `rows`.  Per iteration: one matvec (with the
+// <w_k, A w_k> partials fused into its last kernel when possible), one fused
+// update + norm kernel and two tiny finalisers.  Fully asynchronous on `st`.
 template <class MV>
-static hp_status run_lanczos(const hp_set_s* s, MV&& matvec, const double2* v0, int steps, bool reorth,
-                             LzState* state, double2* partial, double2* V, double2* w, cudaStream_t st) {
+static hp_status run_lanczos(const hp_set_s* s, MV&& matvec, const double2* w0, double2* rows, int steps,
+                             bool reorth, LzState* state, double2* partial, double2* dotbuf, double2* z,
+                             cudaStream_t st) {
   int64_t n = s->n;
   int g = grid_for(n, 256, 148 * 16);
+  auto row = [&](int k) -> double2* { return k == 0 ? const_cast<double2*>(w0) : rows + (int64_t)(k - 1) * n; };
   k_lz_init<<<1, 32, 0, st>>>(state, steps);
   HP_LAUNCH_CHECK("k_lz_init");
-  hp_status rc = reduce(1, n, v0, nullptr, partial, state, 0, 1, 0.0, nullptr, st);
+  hp_status rc = reduce(1, n, w0, nullptr, partial, state, 0, 1, 0.0, nullptr, st);  // nrm0, scale_0
   if (rc) return rc;
-  k_lz_div<<<g, 256, 0, st>>>(n, v0, V, state, 0, 0);
-  HP_LAUNCH_CHECK("k_lz_div");
   for (int k = 0; k < steps; ++k) {
-    double2* vk = V + (int64_t)k * n;
-    rc = matvec(vk, w);
+    const double2* wk = row(k);
+    DotOut dot;
+    dot.partial = dotbuf;
+    dot.capacity = HP_DOT_CAPACITY;
+    rc = matvec(wk, z, &dot);
     if (rc) return rc;
-    rc = reduce(0, n, vk, w, partial, state, k, 0, 0.0, nullptr, st);  // alpha_k
-    if (rc) return rc;
+    if (dot.n > 0) {
+      k_red_final<<<1, HP_RED_THREADS, 0, st>>>(dotbuf, dot.n, state, k, 6, 0.0, nullptr);  // alpha_k
+      HP_LAUNCH_CHECK("k_red_final");
+    } else {
+      rc = reduce(0, n, wk, z, partial, state, k, 6, 0.0, nullptr, st);
+      if (rc) return rc;
+    }
     if (k == steps - 1) break;
-    k_lz_update<<<g, 256, 0, st>>>(n, w, vk, k > 0 ? V + (int64_t)(k - 1) * n : vk, state, k);
-    HP_LAUNCH_CHECK("k_lz_update");
-    if (reorth) {
+    double2* wn = row(k + 1);
+    k_lz_update_s<<<HP_RED_BLOCKS, HP_RED_THREADS, 0, st>>>(n, z, wk, k > 0 ? row(k - 1) : wk, wn, state, k,
+                                                           partial);
+    HP_LAUNCH_CHECK("k_lz_update_s");
+    if (!reorth) {
+      k_red_final<<<1, HP_RED_THREADS, 0, st>>>(partial, HP_RED_BLOCKS, state, k, 7, 1e-14, nullptr);  // beta_k
+      HP_LAUNCH_CHECK("k_red_final");
+    } else {
       for (int j = 0; j <= k; ++j) {
-        rc = reduce(0, n, V + (int64_t)j * n, w, partial, state, j, 3, 0.0, nullptr, st);
+        rc = reduce(0, n, row(j), wn, partial, state, j, 8, 0.0, nullptr, st);
         if (rc) return rc;
       }
-      k_lz_reorth<<<g, 256, 0, st>>>(n, w, V, state, k);
-      HP_LAUNCH_CHECK("k_lz_reorth");
+      k_lz_reorth_s<<<g, 256, 0, st>>>(n, wn, w0, rows, state, k);
+      HP_LAUNCH_CHECK("k_lz_reorth_s");
+      rc = reduce(1, n, wn, nullptr, partial, state, k, 7, 1e-14, nullptr, st);
+      if (rc) return rc;
     }
-    rc = reduce(1, n, w, nullptr, partial, state, k, 2, 1e-14, nullptr, st);  // beta_k
-    if (rc) return rc;
-    k_lz_div<<<g, 256, 0, st>>>(n, w, V + (int64_t)(k + 1) * n, state, k, 1);
-    HP_LAUNCH_CHECK("k_lz_div");
   }
   return HP_OK;
 }
@@ -498,7 +619,7 @@ size_t hp_magnus_workspace_bytes(hp_set_t s, int scheme, const int32_t* d1, int 
   std::vector<double> ones(std::max(n1, n2) + 1, 1.0);
   size_t pb = prog_bytes_for(s, make_terms(s->dim, d1, ones.data(), n1));
   if (scheme == 1 && d2) pb = std::max(pb, prog_bytes_for(s, make_terms(s->dim, d2, ones.data(), n2)));
-  return lz_layout(s, m, scheme, pb).total;
+  return lz_layout(s, m - 1, scheme, pb).total;
 }
 
 hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* d1, const double* c1, int n1, const int32_t* d2,
@@ -520,11 +641,12 @@ hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* d1, const double
     H2.prog = build_program(s->dim, H2.terms, HP_ADD_OSC, nullptr);
     pb = std::max(pb, prog_bytes_for(s, H2.terms));
   }
-  LzLayout L = lz_layout(s, m, scheme, pb);
+  LzLayout L = lz_layout(s, m - 1, scheme, pb);
   if (ws_bytes < L.total) return fail(HP_ERR_NOMEM, "workspace too small for hp_magnus_step");
   char* base = (char*)ws;
   LzState* state = (LzState*)(base + L.off_state);
   double2* partial = (double2*)(base + L.off_partial);
+  double2* dotbuf = (double2*)(base + L.off_dot);
   double2* V = (double2*)(base + L.off_V);
   double2* w = (double2*)(base + L.off_w);
   double2* tmp = (double2*)(base + L.off_tmp);
@@ -533,8 +655,8 @@ hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* d1, const double
   size_t pws_bytes = L.total - L.off_prog;
   double2* yv = (double2*)y;
   double gamma = std::sqrt(3.0) / 12.0 * h;
-  auto mv = [&](const double2* v, double2* out) -> hp_status {
-    if (scheme == 0) return apply_ham_full(H1, v, out, tmp, pws, pws_bytes, st);
+  auto mv = [&](const double2* v, double2* out, DotOut* dot) -> hp_status {
+    if (scheme == 0) return apply_ham_full(H1, v, out, tmp, pws, pws_bytes, st, dot);
     double2 *y1 = g, *y2 = g + n, *z2 = g + 2 * n, *z1 = g + 3 * n;
     hp_status r;
     if ((r = apply_ham_full(H1, v, y1, tmp, pws, pws_bytes, st))) return r;
@@ -545,12 +667,12 @@ hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* d1, const double
     HP_LAUNCH_CHECK("k_gl2_combine");
     return HP_OK;
   };
-  rc = run_lanczos(s, mv, yv, m, reorth != 0, state, partial, V, w, st);
+  rc = run_lanczos(s, mv, yv, V, m, reorth != 0, state, partial, dotbuf, w, st);
   if (rc) return rc;
   k_lz_expm<<<1, 32, 0, st>>>(state, h);
   HP_LAUNCH_CHECK("k_lz_expm");
-  k_lz_combine<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, V, state, yv);
-  HP_LAUNCH_CHECK("k_lz_combine");
+  k_lz_combine_s<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, yv, V, state, yv);
+  HP_LAUNCH_CHECK("k_lz_combine_s");
   if (diag) {
     k_lz_diag<<<1, 32, 0, st>>>(state, diag, nullptr, nullptr);
     HP_LAUNCH_CHECK("k_lz_diag");
@@ -572,15 +694,21 @@ hp_status hp_lanczos(hp_set_t s, const int32_t* d, const double* c, int nterms, 
   char* base = (char*)ws;
   LzState* state = (LzState*)(base + L.off_state);
   double2* partial = (double2*)(base + L.off_partial);
+  double2* dotbuf = (double2*)(base + L.off_dot);
   double2* w = (double2*)(base + L.off_w);
   double2* tmp = (double2*)(base + L.off_tmp);
   double2* pws = (double2*)(base + L.off_prog);
   size_t pws_bytes = L.total - L.off_prog;
-  auto mv = [&](const double2* v, double2* out) -> hp_status {
-    return apply_ham_full(H, v, out, tmp, pws, pws_bytes, st);
+  auto mv = [&](const double2* v, double2* out, DotOut* dot) -> hp_status {
+    return apply_ham_full(H, v, out, tmp, pws, pws_bytes, st, dot);
   };
-  rc = run_lanczos(s, mv, (const double2*)v0, steps, reorth != 0, state, partial, (double2*)basis, w, st);
+  double2* B = (double2*)basis;
+  int64_t n = s->n;
+  HP_CUDA(cudaMemcpyAsync(B, v0, (size_t)n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  rc = run_lanczos(s, mv, B, B + n, steps, reorth != 0, state, partial, dotbuf, w, st);
   if (rc) return rc;
+  k_lz_normalize_rows<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, B, state);
+  HP_LAUNCH_CHECK("k_lz_normalize_rows");
   k_lz_diag<<<1, 32, 0, st>>>(state, diag, alpha, beta);
   HP_LAUNCH_CHECK("k_lz_diag");
   return HP_OK;

@@ -50,9 +50,20 @@ struct Term {
 std::vector<Term> make_terms(int dim, const int32_t* degrees, const double* coeffs, int nterms);
 Program build_program(int dim, const std::vector<Term>& terms, int flags, const int32_t* axis_order);
 
+// Optional fused inner product <v, y> of the matvec input and output
+// (complex, batch 1): the kernel that writes the final y also writes one
+// partial sum per CTA into `partial`; `n` is set to the number written.
+// Used by the Lanczos recurrence to avoid a separate pass over v and y.
+struct DotOut {
+  double2* partial = nullptr;
+  int capacity = 0;
+  int n = 0;
+};
+constexpr int HP_DOT_CAPACITY = 1 << 15;
+
 template <class T>
 hp_status run_program(const hp_set_s* s, const Program& p, double halfwidth, const T* v, T* y,
-                      int64_t batch, T* ws, size_t ws_bytes, cudaStream_t st);
+                      int64_t batch, T* ws, size_t ws_bytes, cudaStream_t st, DotOut* dot = nullptr);
 template <class T>
 hp_status launch_square(const hp_set_s* s, const T* v, T* out, int64_t batch, cudaStream_t st);
 template <class T>
@@ -64,6 +75,35 @@ size_t fullgrid_workspace_bytes(const hp_set_s* s, const std::vector<Term>& term
                                 int64_t batch, int flags);
 hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                          const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
-                         cudaStream_t st, bool* done);
+                         cudaStream_t st, bool* done, DotOut* dot = nullptr);
+
+// block-wide sum of a double2 (blockDim multiple of 32, <= 1024); result valid in thread 0
+__device__ __forceinline__ double2 block_sum2(double2 v) {
+  __shared__ double2 red_sh[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+  }
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red_sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int nw = (blockDim.x + 31) >> 5;
+    v = lane < nw ? red_sh[lane] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+      v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+    }
+  }
+  return v;
+}
+// conj(a) * b accumulated into acc
+__device__ __forceinline__ void cdot_acc(double2 a, double2 b, double2& acc) {
+  acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+}
 
 }  // namespace hp
