@@ -280,4 +280,234 @@ __global__ void __launch_bounds__(512, 1) k_fg_outer2(const double2* __restrict_
   }
 }
 
+// ---------------------------------------------------------------- v3 kernels
+// The march loop is unrolled by FG3_U = 18 = lcm(9, 2, 3) and the smem rings
+// have FG3_U (v / rows) and FG3_NU (u) slots, both dividing the unroll, so
+// every ring slot, window slot and band offset is a compile-time constant;
+// global addresses advance by pointer increments.  This removes most of the
+// integer work per point that bounded the v2 kernels (ncu: IMAD ~ DFMA).
+constexpr int FG3_U = 18;
+constexpr int FG3_DA = 4;   // planes in flight, pass A
+constexpr int FG3_NU = 6;   // u ring slots, pass A (divides FG3_U, >= FG3_DA + 2)
+constexpr int FG3_DB = 8;   // rows in flight, pass B
+constexpr unsigned FG_MASK_PM1 = 0x28;  // diagonals -1, +1
+
+template <unsigned M2, unsigned M3>
+__global__ void __launch_bounds__(128) k_fg_inner3(const double2* __restrict__ v, double2* __restrict__ u,
+                                                   const double* __restrict__ P2, const double* __restrict__ P3,
+                                                   int n2, int n3) {
+  constexpr int U = FG3_U, D = FG3_DB, K = FG_K, W = FG_W;
+  static_assert(U % W == 0 && U >= K + D + 2, "ring / unroll mismatch");
+  extern __shared__ double2 ring[];  // [U][n3 + 2K], pads zero
+  const int t = threadIdx.x;
+  const int RW = n3 + 2 * K;
+  const bool act = t < n3;
+  const int64_t base = (int64_t)blockIdx.x * n2 * n3;
+  const double2* vb = v + base;
+  double2* dst = u + base + t;
+  for (int i = t; i < U * 2 * K; i += blockDim.x) {
+    int slot = i / (2 * K), k = i % (2 * K);
+    ring[slot * RW + (k < K ? k : n3 + k)] = zz();
+  }
+  double p3[W];
+#pragma unroll
+  for (int d = 0; d < W; ++d) p3[d] = ((M3 >> d) & 1) && act ? __ldg(P3 + t * W + d) : 0.0;
+  double2* myring = ring + K + t;
+  auto issue = [&](int slot, const double2* src, bool ok) {
+    if (act) cp_async16(myring + slot * RW, ok ? (const void*)src : (const void*)vb, ok ? 16 : 0);
+  };
+  const double2* src = vb + t;
+#pragma unroll
+  for (int r = 0; r <= K; ++r) issue(r, src + (int64_t)r * n3, r < n2);
+  cp_commit();
+#pragma unroll
+  for (int r = K + 1; r < K + D; ++r) {
+    issue(r, src + (int64_t)r * n3, r < n2);
+    cp_commit();
+  }
+  cp_wait<D - 1>();
+  __syncthreads();
+  double2 V[W];  // slot (q + K) mod W holds row q
+#pragma unroll
+  for (int q = -K - 1; q <= K - 1; ++q) V[((q + K) % W + W) % W] = (act && q >= 0 && q < n2) ? myring[q * RW] : zz();
+  src += (int64_t)(K + D) * n3;
+  const double* p2r = P2;
+  for (int i0 = 0; i0 < n2; i0 += U) {
+    unroll<U>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      const int i = i0 + k;
+      if (i >= n2) return;
+      double p2[W];
+#pragma unroll
+      for (int d = 0; d < W; ++d) p2[d] = ((M2 >> d) & 1) ? __ldg(p2r + d) : 0.0;
+      p2r += W;
+      issue((k + K + D) % U, src, i + K + D < n2);
+      src += n3;
+      cp_commit();
+      cp_wait<D>();
+      __syncthreads();
+      V[(k + 2 * K) % W] = act ? myring[((k + K) % U) * RW] : zz();
+      if (act) {
+        const double2* row = myring + (k % U) * RW - K;  // row[d] = element j4 + d - K of row i
+        double2 acc = zz(), acc2 = zz();
+#pragma unroll
+        for (int d = 0; d < W; ++d) {
+          if ((M2 >> d) & 1) fma2(p2[d], V[(k + d) % W], acc);
+          if (d != K && ((M3 >> d) & 1)) fma2(p3[d], row[d], acc2);
+        }
+        fma2(p3[K], V[(k + K) % W], acc2);
+        *dst = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+      }
+      dst += n3;
+    });
+  }
+  cp_wait<0>();
+}
+
+template <int RM, int NMIX, unsigned M0, unsigned M1P, unsigned M1G>
+__global__ void __launch_bounds__(512, 1) k_fg_outer3(const double2* __restrict__ v, const double2* __restrict__ u,
+                                                      double2* __restrict__ y, const double* __restrict__ P0,
+                                                      const double* __restrict__ P1, const double* __restrict__ G,
+                                                      const double* __restrict__ B0, int n0, int n1, int64_t S0,
+                                                      int64_t S1, int r0a, int r0b, double2* __restrict__ dotp) {
+  constexpr int U = FG3_U, D = FG3_DA, NU = FG3_NU, K = FG_K, W = FG_W;
+  constexpr int WS = RM + 1, WG = 2 * RM + 1;
+  constexpr int NM = NMIX > 0 ? NMIX : 1;
+  static_assert(U % W == 0 && U % WS == 0 && U % WG == 0 && U % NU == 0, "unroll must cover every ring");
+  static_assert(U >= K + D + 2 && NU >= D + 2, "ring too short for the prefetch distance");
+  extern __shared__ double2 sm[];
+  const int tile = n1 * FG_C;
+  const int SL = (n1 + 2 * K) * FG_C;
+  const int t = threadIdx.x;
+  const bool act = t < tile;
+  const int j1 = t / FG_C, e = t % FG_C;
+  const int64_t off = (int64_t)j1 * S1 + (int64_t)blockIdx.x * FG_C + e;
+  double2* myring = sm + (K + j1) * FG_C + e;  // my element in ring slot 0
+  double2* myu = sm + U * SL + t;              // my element in u-ring slot 0
+  for (int i = t; i < U * 2 * K * FG_C; i += blockDim.x) {
+    int slot = i / (2 * K * FG_C), k = i % (2 * K * FG_C);
+    sm[slot * SL + (k < K * FG_C ? k : tile + k)] = zz();
+  }
+  double p1[W], g[NM][W];
+#pragma unroll
+  for (int d = 0; d < W; ++d) {
+    p1[d] = act && ((M1P >> d) & 1) ? __ldg(P1 + j1 * W + d) : 0.0;
+#pragma unroll
+    for (int m = 0; m < NM; ++m)
+      g[m][d] = act && m < NMIX && ((M1G >> d) & 1) ? __ldg(G + (size_t)m * FG_MAXN * W + j1 * W + d) : 0.0;
+  }
+  const double2* vs = v + off;
+  const double2* us = u + off;
+  auto issue_v = [&](int slot, const double2* src, bool ok) {
+    if (act) cp_async16(myring + slot * SL, ok ? (const void*)src : (const void*)v, ok ? 16 : 0);
+  };
+  auto issue_u = [&](int slot, const double2* src, bool ok) {
+    if (act) cp_async16(myu + slot * tile, ok ? (const void*)src : (const void*)u, ok ? 16 : 0);
+  };
+#pragma unroll
+  for (int p = 0; p <= K; ++p) issue_v(p, vs + (int64_t)p * S0, p < n0);
+  issue_u(0, us, 0 < n0);
+  cp_commit();
+#pragma unroll
+  for (int k = 1; k < D; ++k) {
+    issue_v(K + k, vs + (int64_t)(K + k) * S0, K + k < n0);
+    issue_u(k, us + (int64_t)k * S0, k < n0);
+    cp_commit();
+  }
+  cp_wait<D - 1>();
+  __syncthreads();
+
+  // j2 bands of the ring plane in `slot`: s1 = P_1 v(q), gm = G_m v(q)
+  auto exchange = [&](int slot, bool valid, double2& s1, double2 (&gm)[NM]) {
+    s1 = zz();
+#pragma unroll
+    for (int m = 0; m < NM; ++m) gm[m] = zz();
+    if (!valid || !act) return;
+    const double2* pl = myring + slot * SL;
+#pragma unroll
+    for (int d = 0; d < W; ++d) {
+      constexpr unsigned any = M1P | M1G;
+      if (!((any >> d) & 1)) continue;
+      double2 x = pl[(d - K) * FG_C];
+      if ((M1P >> d) & 1) fma2(p1[d], x, s1);
+      if ((M1G >> d) & 1)
+#pragma unroll
+        for (int m = 0; m < NMIX; ++m) fma2(g[m][d], x, gm[m]);
+    }
+  };
+
+  double2 V[W], S1W[WS], GW[NM][WG];
+#pragma unroll
+  for (int q = -K - 1; q <= K - 1; ++q)
+    V[((q + K) % W + W) % W] = (act && q >= 0 && q < n0) ? myring[q * SL] : zz();
+#pragma unroll
+  for (int q = -RM - 1; q <= RM - 1; ++q) {
+    double2 s1, gm[NM];
+    exchange(q < 0 ? 0 : q, q >= 0 && q < n0, s1, gm);
+    if (q >= -1) S1W[((q % WS) + WS) % WS] = s1;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) GW[m][(((q + RM) % WG) + WG) % WG] = gm[m];
+  }
+  double2 dacc = zz();
+  const double2* vnext = vs + (int64_t)(K + D) * S0;
+  const double2* unext = us + (int64_t)D * S0;
+  double2* yp = y + off;
+  const double* p0r = P0;
+  const double* b0r[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) b0r[m] = B0 + (size_t)(m == 0 ? r0a : r0b) * n0 * W + K;
+  for (int p0 = 0; p0 < n0; p0 += U) {
+    unroll<U>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      const int p = p0 + k;
+      if (p >= n0) return;
+      double t0[W], tb[NM][WG];
+#pragma unroll
+      for (int d = 0; d < W; ++d) t0[d] = ((M0 >> d) & 1) ? __ldg(p0r + d) : 0.0;
+      p0r += W;
+#pragma unroll
+      for (int m = 0; m < NMIX; ++m) {
+#pragma unroll
+        for (int d = -RM; d <= RM; ++d) tb[m][d + RM] = __ldg(b0r[m] + d);
+        b0r[m] += W;
+      }
+      issue_v((k + K + D) % U, vnext, p + K + D < n0);
+      issue_u((k + D) % NU, unext, p + D < n0);
+      vnext += S0;
+      unext += S0;
+      cp_commit();
+      cp_wait<D>();
+      __syncthreads();
+      V[(k + 2 * K) % W] = (act && p + K < n0) ? myring[((k + K) % U) * SL] : zz();
+      {
+        double2 s1, gm[NM];
+        exchange((k + RM) % U, p + RM < n0, s1, gm);
+        S1W[(k + RM) % WS] = s1;
+#pragma unroll
+        for (int m = 0; m < NM; ++m) GW[m][(k + 2 * RM) % WG] = gm[m];
+      }
+      if (act) {
+        double2 acc = myu[(k % NU) * tile];
+        double2 acc2 = S1W[k % WS];
+#pragma unroll
+        for (int d = 0; d < W; ++d)
+          if ((M0 >> d) & 1) fma2(t0[d], V[(k + d) % W], (d & 2) ? acc : acc2);
+#pragma unroll
+        for (int m = 0; m < NMIX; ++m)
+#pragma unroll
+          for (int d = -RM; d <= RM; ++d) fma2(tb[m][d + RM], GW[m][(k + d + RM) % WG], acc);
+        const double2 out = make_double2(acc.x + acc2.x, acc.y + acc2.y);
+        *yp = out;
+        if (dotp) cdot_acc(V[(k + K) % W], out, dacc);
+      }
+      yp += S0;
+    });
+  }
+  cp_wait<0>();
+  if (dotp) {
+    dacc = block_sum2(dacc);
+    if (t == 0) dotp[blockIdx.x] = dacc;
+  }
+}
+
 }  // namespace hp
