@@ -578,7 +578,13 @@ size_t hp_poly_workspace_bytes(hp_set_t s, const int32_t* degrees, int nterms, i
   // large batches run in chunks whose trie workspace stays below kChunkCap
   int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(kChunkCap / std::max<size_t>(per_vec, 1))));
   size_t gen = per_vec * chunk;
-  return std::max(gen, fg);
+  size_t lv = 0;
+  if (!(flags & HP_REF_ORDER)) {
+    // level-fused evaluator: its child vectors for one (chunk of the) batch
+    size_t lv1 = level_workspace_bytes(s, terms, dtype, 1);
+    if (lv1) lv = lv1 * std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(kChunkCap / lv1)));
+  }
+  return std::max(std::max(gen, fg), lv);
 }
 
 hp_status hp_apply_polynomial(hp_set_t s, const int32_t* degrees, const double* coeffs, int nterms,
@@ -601,6 +607,10 @@ hp_status hp_apply_polynomial(hp_set_t s, const int32_t* degrees, const double* 
   if (!(flags & HP_REF_ORDER) && !axis_order) {
     rc = fullgrid_apply(s, terms, halfwidth, dtype, in, out, batch, flags, ws, ws_bytes, st, &done);
     if (rc) return rc;
+    if (!done) {
+      rc = level_apply(s, terms, halfwidth, dtype, in, out, batch, flags, ws, ws_bytes, st, &done);
+      if (rc) return rc;
+    }
   }
   if (!done) {
     Program p = build_program(s->dim, terms, flags, axis_order);

@@ -384,6 +384,10 @@ __device__ bool expm_col(int m, const double* alpha, const double* beta, double 
   return true;
 }
 
+}  // namespace hp
+#include "hp_small.cuh"
+namespace hp {
+
 __global__ void k_lz_expm(LzState* st, double tau) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (!expm_col(st->m_eff, st->alpha, st->beta, tau, st->col)) st->ql_fail = 1;
@@ -459,6 +463,8 @@ static hp_status apply_ham(const Hamiltonian& H, const double2* v, double2* y, d
   hp_status rc = fullgrid_apply(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done,
                                 dot);
   if (rc) return rc;
+  if (!done) rc = level_apply(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done, dot);
+  if (rc) return rc;
   if (!done) rc = run_program<double2>(H.s, H.prog, H.halfwidth, v, y, 1, ws, ws_bytes, st, dot);
   return rc;
 }
@@ -513,7 +519,8 @@ static size_t prog_bytes_for(const hp_set_s* s, const std::vector<Term>& terms) 
   Program p = build_program(s->dim, terms, HP_ADD_OSC, nullptr);
   size_t gen = (size_t)std::max(p.nslots, 1) * s->n * 16;
   size_t fg = fullgrid_workspace_bytes(s, terms, HP_C128, 1, HP_ADD_OSC);
-  return std::max(gen, fg);
+  size_t lv = level_workspace_bytes(s, terms, HP_C128, 1);
+  return std::max(std::max(gen, fg), lv);
 }
 
 // Scaled Lanczos recurrence (krylov_propagator.py:58-104) for `steps`
@@ -655,6 +662,12 @@ hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* d1, const double
   size_t pws_bytes = L.total - L.off_prog;
   double2* yv = (double2*)y;
   double gamma = std::sqrt(3.0) / 12.0 * h;
+  if (scheme == 0 && q == 0.0 && !reorth) {
+    // small sets: the whole step in one launch (hp_small.cuh)
+    bool done = false;
+    rc = small_magnus_step(s, H1.prog, halfwidth, h, m, yv, diag, V, w, pws, pws_bytes, st, &done);
+    if (rc || done) return rc;
+  }
   auto mv = [&](const double2* v, double2* out, DotOut* dot) -> hp_status {
     if (scheme == 0) return apply_ham_full(H1, v, out, tmp, pws, pws_bytes, st, dot);
     double2 *y1 = g, *y2 = g + n, *z2 = g + 2 * n, *z1 = g + 3 * n;

@@ -77,6 +77,12 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
                          const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
                          cudaStream_t st, bool* done, DotOut* dot = nullptr);
 
+// level-fused evaluator (hp_level.cu): complex vectors, degrees <= 4
+size_t level_workspace_bytes(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch);
+hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
+                      const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
+                      cudaStream_t st, bool* done, DotOut* dot = nullptr);
+
 // block-wide sum of a double2 (blockDim multiple of 32, <= 1024); result valid in thread 0
 __device__ __forceinline__ double2 block_sum2(double2 v) {
   __shared__ double2 red_sh[32];
