@@ -157,12 +157,13 @@ def _cpu_worker(args):
     return appl.n * nvec, times
 
 
-def cpu_plan(wname: str, workers: int):
-    """Bounded sample per worker: cfg4 -> a 12-plane j1 slab (25.2M coefficients) of the real cube."""
+def cpu_plan(wname: str, workers: int, planes: int = 12):
+    """Bounded sample per worker: cfg4 -> a `planes`-plane j1 slab of the real cube."""
     if wname == "cfg4":
-        samples = [{"planes": (8 * i, 8 * i + 12)} for i in range(workers)]
-        desc = ("hprop numpy algorithm (oracle port) on 12-plane j1 slabs of the cfg4 cube "
-                "(25.2M coefficients each, one slab per worker); rate = slab coefficients / time")
+        samples = [{"planes": (min(8 * i, 128 - planes), min(8 * i, 128 - planes) + planes)} for i in range(workers)]
+        desc = (f"hprop numpy algorithm (oracle port) on {planes}-plane j1 slabs of the cfg4 cube "
+                f"({planes * 2.097152:.1f}M coefficients each, one slab per worker process); "
+                "rate = slab coefficients / time (a whole-cube run has the same per-coefficient work)")
     elif wname == "cfg3":
         samples = [{"bound": 1023}] * workers
         desc = "oracle port on build_hyperbolic(6,1023) (611,556 coeffs, same W) -- scaled sample of cfg3"
@@ -175,8 +176,8 @@ def cpu_plan(wname: str, workers: int):
     return samples, desc
 
 
-def run_cpu(wname: str, workers: int, reps: int):
-    samples, desc = cpu_plan(wname, workers)
+def run_cpu(wname: str, workers: int, reps: int, planes: int = 12):
+    samples, desc = cpu_plan(wname, workers, planes)
     t0 = time.perf_counter()
     if workers == 1:
         res = [_cpu_worker((wname, samples[0], reps))]
@@ -212,7 +213,9 @@ def reference_arm(args, rank):
         return
     workers = cpu_workers_for(args.workload)
     reps = max(1, args.steps)
-    base = run_cpu(args.workload, workers, reps)
+    # each step is a bounded sample (a 4-plane slab, ~8.4M coefficients per worker, a few
+    # seconds) so that --steps K --warmup W finishes within a few minutes
+    base = run_cpu(args.workload, workers, reps, planes=4)
     line = {"impl": "reference", "metric": "Galerkin matvec throughput", "value": base["value"],
             "unit": "coeffs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": base["seconds_per_rep"] * 1e3, "higher_is_better": True, "scaling": "weak",

@@ -82,8 +82,8 @@ __device__ double2 block_sum_partials(const double2* partial, int np) {
   return sh[0];
 }
 
-// what: 0 alpha_k (dot), 1 nrm0 (norm), 2 beta_k (norm + breakdown), 3 reo[k] (dot),
-//       4 write dot to out[0..1], 5 write norm to out[0]
+// what: 1 nrm0 and scale_0 (norm), 4 write dot to out[0..1], 5 write norm to out[0],
+//       6 alpha_k (scaled dot), 7 beta_k / scale_{k+1} / breakdown (norm), 8 reorth coefficient
 __global__ void __launch_bounds__(HP_RED_THREADS) k_red_final(const double2* partial, int np, LzState* st,
                                                               int k, int what, double tol, double* out) {
   double2 s = block_sum_partials(partial, np);
@@ -91,10 +91,7 @@ __global__ void __launch_bounds__(HP_RED_THREADS) k_red_final(const double2* par
   if (what == 4) { out[0] = s.x; out[1] = s.y; return; }
   if (what == 5) { out[0] = sqrt(s.x); return; }
   if (st->broken && k >= st->m_eff) return;
-  if (what == 0) {
-    st->alpha[k] = s.x;
-    st->defect = fmax(st->defect, fabs(s.y));
-  } else if (what == 6) {  // alpha_k = s_k^2 <w_k, A w_k>
+  if (what == 6) {  // alpha_k = s_k^2 <w_k, A w_k>
     double s2 = st->scale[k] * st->scale[k];
     st->alpha[k] = s2 * s.x;
     st->defect = fmax(st->defect, fabs(s2 * s.y));
@@ -113,18 +110,6 @@ __global__ void __launch_bounds__(HP_RED_THREADS) k_red_final(const double2* par
   } else if (what == 1) {
     st->nrm0 = sqrt(s.x);
     st->scale[0] = 1.0 / st->nrm0;
-  } else if (what == 2) {
-    double bk = sqrt(s.x);
-    st->scratch = bk;
-    if (bk <= tol) {
-      st->broken = 1;
-      st->m_eff = k + 1;
-      st->breakdown_at = k + 1;
-    } else {
-      st->beta[k] = bk;
-    }
-  } else if (what == 3) {
-    st->reo[k] = s;
   }
 }
 
@@ -140,44 +125,6 @@ static hp_status reduce(int mode, int64_t n, const double2* a, const double2* b,
 
 // ---------------------------------------------------------------- vector kernels
 
-// dst = src / (which == 0 ? nrm0 : beta[k])   (krylov_propagator.py:72, 95)
-__global__ void k_lz_div(int64_t n, const double2* __restrict__ src, double2* __restrict__ dst,
-                         const LzState* st, int k, int which) {
-  if (which == 1 && st->broken && k >= st->m_eff - 1) return;
-  double d = which == 0 ? st->nrm0 : st->beta[k];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = sdiv(__ldg(src + i), d);
-}
-
-// w = (w - alpha_k v_k) - beta_{k-1} v_{k-1}   (krylov_propagator.py:86)
-__global__ void k_lz_update(int64_t n, double2* __restrict__ w, const double2* __restrict__ vk,
-                            const double2* __restrict__ vprev, const LzState* st, int k) {
-  if (st->broken && k >= st->m_eff) return;
-  double al = st->alpha[k];
-  double bp = k > 0 ? st->beta[k - 1] : 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double2 t = ssub(w[i], smul(al, __ldg(vk + i)));
-    if (k > 0) t = ssub(t, smul(bp, __ldg(vprev + i)));
-    w[i] = t;
-  }
-}
-
-// full reorthogonalisation: w -= sum_{j<=k} reo[j] v_j   (krylov_propagator.py:87-88)
-__global__ void k_lz_reorth(int64_t n, double2* __restrict__ w, const double2* __restrict__ V, const LzState* st,
-                            int k) {
-  if (st->broken && k >= st->m_eff) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int j = 0; j <= k; ++j) {
-      double2 c = st->reo[j];
-      double2 v = __ldg(V + (int64_t)j * n + i);
-      acc.x += c.x * v.x - c.y * v.y;
-      acc.y += c.x * v.y + c.y * v.x;
-    }
-    w[i] = ssub(w[i], acc);
-  }
-}
-
 // gl2 operator average: out = 0.5 (y1 + y2) - i gamma (z2 - z1)  (krylov_propagator.py:226-231)
 __global__ void k_gl2_combine(int64_t n, const double2* __restrict__ y1, const double2* __restrict__ y2,
                               const double2* __restrict__ z2y1, const double2* __restrict__ z1y2, double gamma,
@@ -188,22 +135,6 @@ __global__ void k_gl2_combine(int64_t n, const double2* __restrict__ y1, const d
     double2 ic = make_double2(__dsub_rn(__dmul_rn(0.0, c.x), __dmul_rn(gamma, c.y)),
                               __dadd_rn(__dmul_rn(0.0, c.y), __dmul_rn(gamma, c.x)));
     out[i] = ssub(h, ic);
-  }
-}
-
-// y = nrm0 * sum_{k < m_eff} col_k v_k   (krylov_propagator.py:186)
-__global__ void k_lz_combine(int64_t n, const double2* __restrict__ V, const LzState* st, double2* __restrict__ y) {
-  int m = st->m_eff;
-  double s = st->nrm0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int k = 0; k < m; ++k) {
-      double2 c = st->col[k];
-      double2 v = __ldg(V + (int64_t)k * n + i);
-      acc.x += v.x * c.x - v.y * c.y;
-      acc.y += v.x * c.y + v.y * c.x;
-    }
-    y[i] = make_double2(s * acc.x, s * acc.y);
   }
 }
 
