@@ -242,7 +242,7 @@ def gpu_arm(args, rank, world, local_rank):
     hbm = float(peaks["hbm_gbs"])
 
     sharding = None
-    if world > 1 and w.kind == "full" and w.batch == 1:
+    if (world > 1 or args.force_shard) and w.kind == "full" and w.batch == 1:
         from paper_1403_3511_b200 import sharding as SH
 
         sharding = SH.SlabShard(w.dim, w.bound, rank, world, halo=w.degree)
@@ -376,6 +376,8 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--force-shard", action="store_true",
+                    help="run the slab-sharded code path even at one rank (tests the N>1 path's local part)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
