@@ -1,23 +1,25 @@
-// Level-fused evaluator: one kernel per axis level of the suffix trie.
+// Level-fused evaluator: one kernel per axis level, suffix trie + prefix Clenshaw.
 //
-// The suffix trie (hp_apply.cu) runs one kernel per Chebyshev *step*; every
-// step re-reads its input through the neighbour tables, writes a vector and
-// read-modify-writes y for each harvested term (~90 B per coefficient per
-// step, 32 steps for cfg3).  Here every trie level -- all nodes that apply
-// axis a, all their degrees, all their harvests -- is ONE kernel:
+// The surrogate y = sum_r alpha_r T_{r_1}(X_1) ... T_{r_N}(X_N) v is
+// evaluated axis by axis, innermost axis first (the reference's product
+// order, fast_apply.py:166-193).  Each level a is ONE kernel: for every
+// ordinal o it walks the axis-a line through o to +-K (K = largest degree
+// at this level) via the neighbour tables (down-chains never break in a
+// downward-closed set; up-chains stop at the first pruned index), and runs
+// the three-term recurrence T_k = (2/L) X T_{k-1} - T_{k-2} on the shrinking
+// window in registers with absent positions forced to zero -- so T_k(X_a) x
+// at o is exactly the restricted operator of fast_apply.py:69-92 -- and
+// accumulates "targets": each target is a linear combination
+// sum_e w_e T_{k_e}(X_a) x_{i_e}, written once per level.
 //
-//   for each ordinal o: walk the axis-a line through o to +-K (K = largest
-//   degree at this level) via the neighbour tables (down-chains never break
-//   in a downward-closed set; up-chains stop at the first pruned index),
-//   load each input node vector on that segment, run the three-term
-//   recurrence T_k = (2/L) X T_{k-1} - T_{k-2} on the shrinking window
-//   (K^2 tiny evaluations in registers, absent positions forced to zero, so
-//   T_k(o) is exactly the restricted operator of fast_apply.py:69-92), then
-//   write the child vectors the next level needs and accumulate every
-//   harvested term into y with a single read-modify-write per level.
-//
-// Product order inside each term (axis N first) is unchanged, so on pruned
-// sets the operator is the reference's; only summation order differs.
+// Levels N-1 .. c+1 run in suffix mode (targets = child vectors
+// T_k(X_a) u_sigma that share trailing degrees, plus y for finished terms);
+// level c forms prefix vectors z_pi = sum alpha T_{r_c}(X_c) u_sigma grouped by
+// the degrees still to apply on axes 0..c-1; levels c-1 .. 0 run in prefix
+// (Clenshaw) mode, z'_pi' = sum_k T_k(X_a) z_(pi',k).  The planner picks the
+// cut c that minimises the vectors read and written.  Product order inside
+// every term is unchanged, so on pruned sets the operator is the
+// reference's; only the summation order of the terms differs.
 #include <algorithm>
 #include <map>
 #include <vector>
@@ -27,124 +29,235 @@
 
 namespace hp {
 
-constexpr int LV_MAXIN = 48;
-constexpr int LV_MAXACT = 10;
+constexpr int LV_MAXIN = 64;
+constexpr int LV_MAXTG = 64;
+constexpr int LV_MAXENT = 160;
 constexpr int LV_MAXK = 4;
 
-struct LvAct {
-  signed char k;      // degree
-  signed char child;  // >= 0: write T_k into slot `child`; -1: acc += w * T_k
+struct LvEnt {
+  unsigned char input;  // index into in_buf
+  signed char k;        // degree
   double w;
 };
 
 struct LvLevel {
   int axis;
   int K;
-  int nin;
-  short in_buf[LV_MAXIN];  // -2 = v, >= 0 slot
-  unsigned char nact[LV_MAXIN];
-  LvAct act[LV_MAXIN][LV_MAXACT];
+  int nin, ntg;
+  short in_buf[LV_MAXIN];   // -2 = v, >= 0 slot
+  short tg_buf[LV_MAXTG];   // -1 = y, >= 0 slot
+  short tg_start[LV_MAXTG + 1];
+  LvEnt ent[LV_MAXENT];     // grouped by target, sorted by input inside a target
 };
 
 struct LvProgram {
   std::vector<LvLevel> levels;
   int nslots = 0;
   bool ok = false;
+  double cost = 0.0;
 };
 
 // ---------------------------------------------------------------- planner
 
-static LvProgram plan_levels(int dim, const std::vector<Term>& terms) {
+namespace {
+
+struct Builder {
+  LvLevel L{};
+  std::map<int, int> in_index;                        // buffer -> input index
+  std::map<int, std::vector<std::pair<int, LvEnt>>> tg;  // target buffer -> (order, entry)
+  bool ok = true;
+  int input(int buf) {
+    auto it = in_index.find(buf);
+    if (it != in_index.end()) return it->second;
+    if (L.nin >= LV_MAXIN) { ok = false; return 0; }
+    in_index[buf] = L.nin;
+    L.in_buf[L.nin] = (short)buf;
+    return L.nin++;
+  }
+  void add(int target_buf, int in_buf, int k, double w) {
+    LvEnt e;
+    e.input = (unsigned char)input(in_buf);
+    e.k = (signed char)k;
+    e.w = w;
+    L.K = std::max(L.K, k);
+    tg[target_buf].push_back({(int)tg[target_buf].size(), e});
+  }
+  bool finish() {
+    if (!ok) return false;
+    if ((int)tg.size() > LV_MAXTG) return false;
+    int ne = 0;
+    L.ntg = 0;
+    for (auto& t : tg) {
+      auto v = t.second;
+      std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.second.input < b.second.input; });
+      L.tg_buf[L.ntg] = (short)t.first;
+      L.tg_start[L.ntg] = (short)ne;
+      for (auto& e : v) {
+        if (ne >= LV_MAXENT) return false;
+        L.ent[ne++] = e.second;
+      }
+      ++L.ntg;
+    }
+    L.tg_start[L.ntg] = (short)ne;
+    return true;
+  }
+};
+
+}  // namespace
+
+static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut) {
   LvProgram P;
+  const int BUF_V_ = -2, BUF_Y_ = -1;
+  int next_slot = 0;
+  std::vector<int> free_slots;
+  auto alloc = [&](const std::vector<int>& avoid) {
+    for (size_t i = 0; i < free_slots.size(); ++i)
+      if (std::find(avoid.begin(), avoid.end(), free_slots[i]) == avoid.end()) {
+        int s = free_slots[i];
+        free_slots.erase(free_slots.begin() + i);
+        return s;
+      }
+    return next_slot++;
+  };
+  auto zero_upto = [&](const Term& t, int upto) {
+    for (int l = 0; l <= upto; ++l)
+      if (t.r[l] != 0) return false;
+    return true;
+  };
+  // suffix nodes: (buffer, terms that still need axes <= a)
   struct Node {
     int buf;
     std::vector<int> rows;
   };
-  std::vector<Node> nodes{{-2, {}}};
-  for (size_t i = 0; i < terms.size(); ++i) nodes[0].rows.push_back((int)i);
-  std::vector<int> free_slots;
-  int next_slot = 0;
-  auto all_zero = [&](int it, int upto) {  // r[0..upto] all zero (upto < 0: true)
-    for (int l = 0; l <= upto; ++l)
-      if (terms[it].r[l] != 0) return false;
-    return true;
-  };
-  for (int a = dim - 1; a >= 0; --a) {
-    LvLevel L{};
-    L.axis = a;
-    L.K = 0;
-    L.nin = 0;
+  std::vector<Node> nodes{{BUF_V_, {}}};
+  bool y_written = false;
+  double cost = 0.0;
+  // terms with all degrees zero: harvested at the first level
+  std::vector<int> consts;
+  for (size_t i = 0; i < terms.size(); ++i) {
+    if (zero_upto(terms[i], dim - 1)) consts.push_back((int)i);
+    else nodes[0].rows.push_back((int)i);
+  }
+  for (int a = dim - 1; a > cut; --a) {  // ---- suffix levels
+    Builder B;
+    B.L.axis = a;
+    std::vector<int> inputs;
+    for (auto& nd : nodes) if (nd.buf >= 0) inputs.push_back(nd.buf);
+    if (!y_written) for (int it : consts) B.add(BUF_Y_, BUF_V_, 0, terms[it].alpha);
     std::vector<Node> next;
-    std::vector<int> in_use;  // slots read at this level (children must not alias them)
-    for (auto& nd : nodes) if (nd.buf >= 0) in_use.push_back(nd.buf);
     std::vector<int> released;
     for (auto& nd : nodes) {
-      if ((int)L.nin >= LV_MAXIN) return P;
-      int ii = L.nin++;
-      L.in_buf[ii] = (short)nd.buf;
-      L.nact[ii] = 0;
       std::map<int, std::vector<int>> groups;
       std::vector<int> pass;
       for (int it : nd.rows) {
         int k = terms[it].r[a];
         if (k > LV_MAXK) return P;
-        if (k == 0 && !all_zero(it, a - 1)) pass.push_back(it);
+        if (k == 0) pass.push_back(it);  // cannot be a leaf: some r[0..a-1] != 0
         else groups[k].push_back(it);
       }
       for (auto& g : groups) {
         int k = g.first;
-        double w = 0.0;
-        bool has_leaf = false;
         std::vector<int> nonleaf;
         for (int it : g.second) {
-          if (all_zero(it, a - 1)) {
-            w += terms[it].alpha;
-            has_leaf = true;
-          } else {
-            nonleaf.push_back(it);
-          }
-        }
-        if (has_leaf) {
-          if (L.nact[ii] >= LV_MAXACT) return P;
-          L.act[ii][L.nact[ii]++] = LvAct{(signed char)k, -1, w};
-          L.K = std::max(L.K, k);
+          if (zero_upto(terms[it], a - 1)) B.add(BUF_Y_, nd.buf, k, terms[it].alpha);
+          else nonleaf.push_back(it);
         }
         if (!nonleaf.empty()) {
-          if (k == 0) return P;  // cannot happen (k == 0 non-leaves pass through)
-          int slot;
-          // a fresh slot, never one this level reads
-          auto it = std::find_if(free_slots.begin(), free_slots.end(),
-                                 [&](int s) { return std::find(in_use.begin(), in_use.end(), s) == in_use.end(); });
-          if (it != free_slots.end()) {
-            slot = *it;
-            free_slots.erase(it);
-          } else {
-            slot = next_slot++;
-          }
-          if (L.nact[ii] >= LV_MAXACT || slot > 120) return P;
-          L.act[ii][L.nact[ii]++] = LvAct{(signed char)k, (signed char)slot, 0.0};
-          L.K = std::max(L.K, k);
-          next.push_back({slot, nonleaf});
+          int s = alloc(inputs);
+          B.add(s, nd.buf, k, 1.0);
+          next.push_back({s, nonleaf});
         }
       }
-      if (L.nact[ii] == 0) --L.nin;  // pass-through only: nothing to read at this level
       if (!pass.empty()) next.push_back({nd.buf, pass});
       else if (nd.buf >= 0) released.push_back(nd.buf);
     }
-    if (L.nin > 0) P.levels.push_back(L);
+    if (!B.finish()) return P;
+    if (B.L.ntg > 0) {
+      if (B.tg.count(BUF_Y_)) y_written = true;
+      cost += B.L.nin + B.L.ntg + (B.tg.count(BUF_Y_) && P.levels.size() ? 1 : 0);
+      P.levels.push_back(B.L);
+    }
     for (int s : released) free_slots.push_back(s);
     nodes = next;
-    if (nodes.empty()) break;
   }
-  if (!nodes.empty()) return P;  // unreachable: axis 0 harvests everything
-  if (P.levels.empty()) {        // no terms: one empty level still writes y (= levels * v)
-    LvLevel L{};
-    L.axis = 0;
-    P.levels.push_back(L);
+  // ---- cut level: z_pi = sum alpha T_{r_cut}(X_cut) u_sigma, pi = (r_0..r_{cut-1})
+  std::map<std::vector<int>, int> zbuf;  // prefix -> slot (empty prefix -> y)
+  {
+    Builder B;
+    B.L.axis = cut;
+    std::vector<int> inputs;
+    for (auto& nd : nodes) if (nd.buf >= 0) inputs.push_back(nd.buf);
+    if (!y_written) for (int it : consts) B.add(BUF_Y_, BUF_V_, 0, terms[it].alpha);
+    for (auto& nd : nodes) {
+      for (int it : nd.rows) {
+        const Term& t = terms[it];
+        if (t.r[cut] > LV_MAXK) return P;
+        std::vector<int> pre(t.r, t.r + cut);
+        bool zero = std::all_of(pre.begin(), pre.end(), [](int x) { return x == 0; });
+        int target;
+        if (zero) target = BUF_Y_;
+        else {
+          auto f = zbuf.find(pre);
+          if (f == zbuf.end()) {
+            target = alloc(inputs);
+            zbuf[pre] = target;
+          } else {
+            target = f->second;
+          }
+        }
+        B.add(target, nd.buf, t.r[cut], t.alpha);
+      }
+    }
+    if (!B.finish()) return P;
+    cost += B.L.nin + B.L.ntg;
+    P.levels.push_back(B.L);
+    for (int s : inputs) free_slots.push_back(s);
   }
+  // ---- prefix levels: z'_pi' = sum_k T_k(X_a) z_(pi',k)
+  for (int a = cut - 1; a >= 0; --a) {
+    Builder B;
+    B.L.axis = a;
+    std::vector<int> inputs;
+    for (auto& z : zbuf) inputs.push_back(z.second);
+    std::map<std::vector<int>, int> nz;
+    for (auto& z : zbuf) {
+      std::vector<int> pre(z.first.begin(), z.first.begin() + a);
+      int k = z.first[a];
+      if (k > LV_MAXK) return P;
+      bool zero = std::all_of(pre.begin(), pre.end(), [](int x) { return x == 0; });
+      int target;
+      if (zero) target = BUF_Y_;
+      else {
+        auto f = nz.find(pre);
+        if (f == nz.end()) {
+          target = alloc(inputs);
+          nz[pre] = target;
+        } else {
+          target = f->second;
+        }
+      }
+      B.add(target, z.second, k, 1.0);
+    }
+    if (!B.finish()) return P;
+    cost += B.L.nin + B.L.ntg + 1;
+    P.levels.push_back(B.L);
+    for (int s : inputs) free_slots.push_back(s);
+    zbuf = nz;
+  }
+  if (!zbuf.empty() || P.levels.empty()) return P;
   P.nslots = next_slot;
+  P.cost = cost + 0.25 * next_slot;
   P.ok = true;
   return P;
+}
+
+static LvProgram plan_levels(int dim, const std::vector<Term>& terms) {
+  LvProgram best;
+  for (int cut = 0; cut < dim; ++cut) {
+    LvProgram P = plan_with_cut(dim, terms, cut);
+    if (P.ok && (!best.ok || P.cost < best.cost)) best = std::move(P);
+  }
+  return best;
 }
 
 // ---------------------------------------------------------------- kernel
@@ -171,9 +284,9 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
 #pragma unroll
       for (int d = 2; d <= K; ++d) {
         int jj;
-        int64_t a0, b0, a1, b1;
-        if (seg[K - d + 1] >= 0) ax.at(seg[K - d + 1], jj, a0, b0); else a0 = -1;
-        if (seg[K + d - 1] >= 0) ax.at(seg[K + d - 1], jj, a1, b1); else b1 = -1;
+        int64_t a0 = -1, b0, a1, b1 = -1;
+        if (seg[K - d + 1] >= 0) ax.at(seg[K - d + 1], jj, a0, b0);
+        if (seg[K + d - 1] >= 0) ax.at(seg[K + d - 1], jj, a1, b1);
         seg[K - d] = a0;
         seg[K + d] = b1;
       }
@@ -190,69 +303,69 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
       for (int a = 0; a < dim; ++a) lev += (double)axs.j(a, o) + 0.5;
     for (int64_t b = 0; b < batch; ++b) {
       const int64_t bo = b * n;
-      double2 acc = make_double2(0.0, 0.0);
-      for (int ii = 0; ii < lv.nin; ++ii) {
-        const double2* x = lv.in_buf[ii] == -2 ? v + bo : slots + (int64_t)lv.in_buf[ii] * n * batch + bo;
-        double2 Tm[S], Tc[S], Tn[S];
+      for (int tgi = 0; tgi < lv.ntg; ++tgi) {
+        double2 acc = make_double2(0.0, 0.0);
+        int last = -1;
+        double2 Tk[K + 1];
+        for (int e = lv.tg_start[tgi]; e < lv.tg_start[tgi + 1]; ++e) {
+          const LvEnt E = lv.ent[e];
+          if (E.input != last) {
+            last = E.input;
+            const int ib = lv.in_buf[E.input];
+            const double2* x = ib == -2 ? v + bo : slots + (int64_t)ib * n * batch + bo;
+            double2 Tm[S], Tc[S], Tn[S];
 #pragma unroll
-        for (int p = 0; p < S; ++p) Tm[p] = seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
-        const int na = lv.nact[ii];
-        // k = 0 actions
-        for (int q = 0; q < na; ++q) {
-          LvAct A = lv.act[ii][q];
-          if (A.k == 0) {
-            acc.x = fma(A.w, Tm[K].x, acc.x);
-            acc.y = fma(A.w, Tm[K].y, acc.y);
-          }
-        }
+            for (int p = 0; p < S; ++p) Tm[p] = seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
+            Tk[0] = Tm[K];
 #pragma unroll
-        for (int k = 1; k <= K; ++k) {
-          const double sc = k == 1 ? inv_L : two_L;
+            for (int k = 1; k <= K; ++k) {
+              const double sc = k == 1 ? inv_L : two_L;
 #pragma unroll
-          for (int p = k; p < S - k; ++p) {
-            const double2 lo = k == 1 ? Tm[p - 1] : Tc[p - 1];
-            const double2 hi = k == 1 ? Tm[p + 1] : Tc[p + 1];
-            double2 r = make_double2(sc * fma(cd[p], lo.x, cu[p] * hi.x), sc * fma(cd[p], lo.y, cu[p] * hi.y));
-            if (k > 1) {
-              r.x -= Tm[p].x;
-              r.y -= Tm[p].y;
-            }
-            if (seg[p] < 0) r = make_double2(0.0, 0.0);
-            Tn[p] = r;
-          }
-          // rotate: (T_{k-2}, T_{k-1}) <- (T_{k-1}, T_k)
-          if (k > 1) {
+              for (int p = k; p < S - k; ++p) {
+                const double2 lo = k == 1 ? Tm[p - 1] : Tc[p - 1];
+                const double2 hi = k == 1 ? Tm[p + 1] : Tc[p + 1];
+                double2 r = make_double2(sc * fma(cd[p], lo.x, cu[p] * hi.x), sc * fma(cd[p], lo.y, cu[p] * hi.y));
+                if (k > 1) {
+                  r.x -= Tm[p].x;
+                  r.y -= Tm[p].y;
+                }
+                if (seg[p] < 0) r = make_double2(0.0, 0.0);
+                Tn[p] = r;
+              }
+              if (k > 1) {
 #pragma unroll
-            for (int p = 0; p < S; ++p) Tm[p] = Tc[p];
-          }
+                for (int p = 0; p < S; ++p) Tm[p] = Tc[p];
+              }
 #pragma unroll
-          for (int p = 0; p < S; ++p) Tc[p] = Tn[p];
-          const double2 val = Tc[K];
-          for (int q = 0; q < na; ++q) {
-            LvAct A = lv.act[ii][q];
-            if (A.k != k) continue;
-            if (A.child >= 0) {
-              slots[(int64_t)A.child * n * batch + bo + o] = val;
-            } else {
-              acc.x = fma(A.w, val.x, acc.x);
-              acc.y = fma(A.w, val.y, acc.y);
+              for (int p = 0; p < S; ++p) Tc[p] = Tn[p];
+              Tk[k] = Tc[K];
             }
           }
+          double2 t = Tk[0];
+#pragma unroll
+          for (int k = 1; k <= K; ++k)
+            if (E.k == k) t = Tk[k];
+          acc.x = fma(E.w, t.x, acc.x);
+          acc.y = fma(E.w, t.y, acc.y);
+        }
+        const int tb = lv.tg_buf[tgi];
+        if (tb >= 0) {
+          slots[(int64_t)tb * n * batch + bo + o] = acc;
+        } else {
+          if (osc) {
+            double2 x = __ldg(v + bo + o);
+            acc.x = fma(lev, x.x, acc.x);
+            acc.y = fma(lev, x.y, acc.y);
+          }
+          if (!first) {
+            double2 old = y[bo + o];
+            acc.x += old.x;
+            acc.y += old.y;
+          }
+          y[bo + o] = acc;
+          if (dotp) cdot_acc(__ldg(v + bo + o), acc, dacc);
         }
       }
-      if (osc) {
-        double2 x = __ldg(v + bo + o);
-        acc.x = fma(lev, x.x, acc.x);
-        acc.y = fma(lev, x.y, acc.y);
-      }
-      double2 out = acc;
-      if (!first) {
-        double2 old = y[bo + o];
-        out.x += old.x;
-        out.y += old.y;
-      }
-      y[bo + o] = out;
-      if (dotp) cdot_acc(__ldg(v + bo + o), out, dacc);
     }
   }
   if (dotp) {
@@ -307,31 +420,40 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
   if (dtype != HP_C128 || (flags & HP_REF_ORDER) || s->n == 0) return HP_OK;
   LvProgram P = plan_levels(s->dim, terms);
   if (!P.ok) return HP_OK;
-  // batches are chunked so that the child vectors fit the workspace
+  // batches are chunked so that the intermediate vectors fit the workspace
   size_t per_vec = (size_t)std::max(P.nslots, 1) * s->n * sizeof(double2);
   int64_t chunk = std::min<int64_t>(batch, (int64_t)(ws_bytes / per_vec));
   if (chunk < 1) return HP_OK;
   const int64_t n = s->n;
   const int grid = grid_for(n, 256, 148 * 8);
   const bool osc = flags & HP_ADD_OSC;
+  // y must be written by the first level that targets it and osc/dot applied at the last
+  int first_y = -1, last_y = -1;
+  for (int li = 0; li < (int)P.levels.size(); ++li)
+    for (int t = 0; t < P.levels[li].ntg; ++t)
+      if (P.levels[li].tg_buf[t] == -1) {
+        if (first_y < 0) first_y = li;
+        last_y = li;
+      }
+  if (first_y < 0) return HP_OK;
   for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
     const int64_t nb = std::min(chunk, batch - b0);
     const double2* v = (const double2*)in + b0 * n;
     double2* y = (double2*)out + b0 * n;
     double2* slots = (double2*)ws;
-    const int nl = (int)P.levels.size();
-    for (int li = 0; li < nl; ++li) {
+    for (int li = 0; li < (int)P.levels.size(); ++li) {
       const LvLevel& lv = P.levels[li];
-      const bool last = li == nl - 1;
-      const int first = li == 0 ? 1 : 0;
+      const bool last = li == last_y;
+      const int first = li == first_y ? 1 : 0;
       double2* dotp = (last && dot && dot->partial && batch == 1 && grid <= dot->capacity) ? dot->partial : nullptr;
       hp_status rc;
+      const int oscf = last && osc ? 1 : 0;
       switch (lv.K) {
-        case 0: rc = launch_level<0>(s, lv, halfwidth, v, slots, y, nb, first, last && osc, dotp, grid, st); break;
-        case 1: rc = launch_level<1>(s, lv, halfwidth, v, slots, y, nb, first, last && osc, dotp, grid, st); break;
-        case 2: rc = launch_level<2>(s, lv, halfwidth, v, slots, y, nb, first, last && osc, dotp, grid, st); break;
-        case 3: rc = launch_level<3>(s, lv, halfwidth, v, slots, y, nb, first, last && osc, dotp, grid, st); break;
-        default: rc = launch_level<4>(s, lv, halfwidth, v, slots, y, nb, first, last && osc, dotp, grid, st); break;
+        case 0: rc = launch_level<0>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
+        case 1: rc = launch_level<1>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
+        case 2: rc = launch_level<2>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
+        case 3: rc = launch_level<3>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
+        default: rc = launch_level<4>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
       }
       if (rc) return rc;
       if (dotp) dot->n = grid;
