@@ -30,12 +30,13 @@
 namespace hp {
 
 constexpr int LV_MAXIN = 64;
-constexpr int LV_MAXTG = 64;
+constexpr int LV_MAXTG = 16;  // targets accumulate in registers
 constexpr int LV_MAXENT = 160;
 constexpr int LV_MAXK = 4;
 
 struct LvEnt {
   unsigned char input;  // index into in_buf
+  unsigned char tg;     // index into tg_buf
   signed char k;        // degree
   double w;
 };
@@ -46,8 +47,8 @@ struct LvLevel {
   int nin, ntg;
   short in_buf[LV_MAXIN];   // -2 = v, >= 0 slot
   short tg_buf[LV_MAXTG];   // -1 = y, >= 0 slot
-  short tg_start[LV_MAXTG + 1];
-  LvEnt ent[LV_MAXENT];     // grouped by target, sorted by input inside a target
+  short in_start[LV_MAXIN + 1];
+  LvEnt ent[LV_MAXENT];     // grouped by input: T_0..T_K of an input are computed once
 };
 
 struct LvProgram {
@@ -85,20 +86,28 @@ struct Builder {
   bool finish() {
     if (!ok) return false;
     if ((int)tg.size() > LV_MAXTG) return false;
-    int ne = 0;
+    std::vector<LvEnt> all;
     L.ntg = 0;
     for (auto& t : tg) {
-      auto v = t.second;
-      std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.second.input < b.second.input; });
       L.tg_buf[L.ntg] = (short)t.first;
-      L.tg_start[L.ntg] = (short)ne;
-      for (auto& e : v) {
-        if (ne >= LV_MAXENT) return false;
-        L.ent[ne++] = e.second;
+      for (auto& e : t.second) {
+        LvEnt x = e.second;
+        x.tg = (unsigned char)L.ntg;
+        all.push_back(x);
       }
       ++L.ntg;
     }
-    L.tg_start[L.ntg] = (short)ne;
+    if ((int)all.size() > LV_MAXENT) return false;
+    std::stable_sort(all.begin(), all.end(), [](const LvEnt& a, const LvEnt& b) { return a.input < b.input; });
+    int ne = 0;
+    for (int i = 0; i < L.nin; ++i) {
+      L.in_start[i] = (short)ne;
+      while (ne < (int)all.size() && all[ne].input == i) {
+        L.ent[ne] = all[ne];
+        ++ne;
+      }
+    }
+    L.in_start[L.nin] = (short)ne;
     return true;
   }
 };
@@ -262,7 +271,7 @@ static LvProgram plan_levels(int dim, const std::vector<Term>& terms) {
 
 // ---------------------------------------------------------------- kernel
 
-template <int K, class AX, class AXS>
+template <int K, int TGN, class AX, class AXS>
 __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, AXS axs, int dim, LvLevel lv,
                                                double inv_L, double two_L, const double2* __restrict__ v,
                                                double2* __restrict__ slots, double2* __restrict__ y, int first,
@@ -303,51 +312,59 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
       for (int a = 0; a < dim; ++a) lev += (double)axs.j(a, o) + 0.5;
     for (int64_t b = 0; b < batch; ++b) {
       const int64_t bo = b * n;
-      for (int tgi = 0; tgi < lv.ntg; ++tgi) {
-        double2 acc = make_double2(0.0, 0.0);
-        int last = -1;
+      double2 accs[TGN];
+#pragma unroll
+      for (int q = 0; q < TGN; ++q) accs[q] = make_double2(0.0, 0.0);
+      for (int ii = 0; ii < lv.nin; ++ii) {
+        // T_0..T_K of this input at o, once
+        const int ib = lv.in_buf[ii];
+        const double2* x = ib == -2 ? v + bo : slots + (int64_t)ib * n * batch + bo;
         double2 Tk[K + 1];
-        for (int e = lv.tg_start[tgi]; e < lv.tg_start[tgi + 1]; ++e) {
-          const LvEnt E = lv.ent[e];
-          if (E.input != last) {
-            last = E.input;
-            const int ib = lv.in_buf[E.input];
-            const double2* x = ib == -2 ? v + bo : slots + (int64_t)ib * n * batch + bo;
-            double2 Tm[S], Tc[S], Tn[S];
+        double2 Tm[S], Tc[S], Tn[S];
 #pragma unroll
-            for (int p = 0; p < S; ++p) Tm[p] = seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
-            Tk[0] = Tm[K];
+        for (int p = 0; p < S; ++p) Tm[p] = seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
+        Tk[0] = Tm[K];
 #pragma unroll
-            for (int k = 1; k <= K; ++k) {
-              const double sc = k == 1 ? inv_L : two_L;
+        for (int k = 1; k <= K; ++k) {
+          const double sc = k == 1 ? inv_L : two_L;
 #pragma unroll
-              for (int p = k; p < S - k; ++p) {
-                const double2 lo = k == 1 ? Tm[p - 1] : Tc[p - 1];
-                const double2 hi = k == 1 ? Tm[p + 1] : Tc[p + 1];
-                double2 r = make_double2(sc * fma(cd[p], lo.x, cu[p] * hi.x), sc * fma(cd[p], lo.y, cu[p] * hi.y));
-                if (k > 1) {
-                  r.x -= Tm[p].x;
-                  r.y -= Tm[p].y;
-                }
-                if (seg[p] < 0) r = make_double2(0.0, 0.0);
-                Tn[p] = r;
-              }
-              if (k > 1) {
-#pragma unroll
-                for (int p = 0; p < S; ++p) Tm[p] = Tc[p];
-              }
-#pragma unroll
-              for (int p = 0; p < S; ++p) Tc[p] = Tn[p];
-              Tk[k] = Tc[K];
+          for (int p = k; p < S - k; ++p) {
+            const double2 lo = k == 1 ? Tm[p - 1] : Tc[p - 1];
+            const double2 hi = k == 1 ? Tm[p + 1] : Tc[p + 1];
+            double2 r = make_double2(sc * fma(cd[p], lo.x, cu[p] * hi.x), sc * fma(cd[p], lo.y, cu[p] * hi.y));
+            if (k > 1) {
+              r.x -= Tm[p].x;
+              r.y -= Tm[p].y;
             }
+            if (seg[p] < 0) r = make_double2(0.0, 0.0);
+            Tn[p] = r;
           }
+          if (k > 1) {
+#pragma unroll
+            for (int p = 0; p < S; ++p) Tm[p] = Tc[p];
+          }
+#pragma unroll
+          for (int p = 0; p < S; ++p) Tc[p] = Tn[p];
+          Tk[k] = Tc[K];
+        }
+        for (int e = lv.in_start[ii]; e < lv.in_start[ii + 1]; ++e) {
+          const LvEnt E = lv.ent[e];
           double2 t = Tk[0];
 #pragma unroll
           for (int k = 1; k <= K; ++k)
             if (E.k == k) t = Tk[k];
-          acc.x = fma(E.w, t.x, acc.x);
-          acc.y = fma(E.w, t.y, acc.y);
+#pragma unroll
+          for (int q = 0; q < TGN; ++q)
+            if (E.tg == q) {
+              accs[q].x = fma(E.w, t.x, accs[q].x);
+              accs[q].y = fma(E.w, t.y, accs[q].y);
+            }
         }
+      }
+#pragma unroll
+      for (int tgi = 0; tgi < TGN; ++tgi) {
+        if (tgi >= lv.ntg) break;
+        double2 acc = accs[tgi];
         const int tb = lv.tg_buf[tgi];
         if (tb >= 0) {
           slots[(int64_t)tb * n * batch + bo + o] = acc;
@@ -391,13 +408,21 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
   if (s->boxed) {
     LvAllBox axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->box(a);
-    k_level<K, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv, 1.0 / L, 2.0 / L,
-                                                     v, slots, y, first, osc, dotp);
+    if (lv.ntg <= 4)
+      k_level<K, 4, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv, 1.0 / L,
+                                                          2.0 / L, v, slots, y, first, osc, dotp);
+    else
+      k_level<K, LV_MAXTG, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv,
+                                                                 1.0 / L, 2.0 / L, v, slots, y, first, osc, dotp);
   } else {
     LvAllTab axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
-    k_level<K, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv, 1.0 / L, 2.0 / L,
-                                                     v, slots, y, first, osc, dotp);
+    if (lv.ntg <= 4)
+      k_level<K, 4, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv, 1.0 / L,
+                                                          2.0 / L, v, slots, y, first, osc, dotp);
+    else
+      k_level<K, LV_MAXTG, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv,
+                                                                 1.0 / L, 2.0 / L, v, slots, y, first, osc, dotp);
   }
   HP_LAUNCH_CHECK("k_level");
   return HP_OK;
