@@ -36,8 +36,9 @@ constexpr int LV_MAXK = 4;
 
 struct LvEnt {
   unsigned char input;  // index into in_buf
-  unsigned char tg;     // index into tg_buf
+  unsigned char tg;     // index into tg_buf (accumulated target), or 0xFF: write w * T_k to `slot`
   signed char k;        // degree
+  short slot;
   double w;
 };
 
@@ -85,14 +86,22 @@ struct Builder {
   }
   bool finish() {
     if (!ok) return false;
-    if ((int)tg.size() > LV_MAXTG) return false;
     std::vector<LvEnt> all;
     L.ntg = 0;
     for (auto& t : tg) {
+      if (t.second.size() == 1 && t.first >= 0) {  // single-term child vector: written directly
+        LvEnt x = t.second[0].second;
+        x.tg = 0xFF;
+        x.slot = (short)t.first;
+        all.push_back(x);
+        continue;
+      }
+      if (L.ntg >= LV_MAXTG) return false;
       L.tg_buf[L.ntg] = (short)t.first;
       for (auto& e : t.second) {
         LvEnt x = e.second;
         x.tg = (unsigned char)L.ntg;
+        x.slot = -1;
         all.push_back(x);
       }
       ++L.ntg;
@@ -262,6 +271,10 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut)
 
 static LvProgram plan_levels(int dim, const std::vector<Term>& terms) {
   LvProgram best;
+  if (const char* e = getenv("HP_LEVEL_CUT")) {  // experiments: force the suffix/prefix cut
+    int c = atoi(e);
+    if (c >= 0 && c < dim) return plan_with_cut(dim, terms, c);
+  }
   for (int cut = 0; cut < dim; ++cut) {
     LvProgram P = plan_with_cut(dim, terms, cut);
     if (P.ok && (!best.ok || P.cost < best.cost)) best = std::move(P);
@@ -319,11 +332,28 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
         // T_0..T_K of this input at o, once
         const int ib = lv.in_buf[ii];
         const double2* x = ib == -2 ? v + bo : slots + (int64_t)ib * n * batch + bo;
-        double2 Tk[K + 1];
+        const int e0 = lv.in_start[ii], e1 = lv.in_start[ii + 1];
+        // entries of this input at degree kk receive t (static indices only: no local memory)
+        auto emit = [&](int kk, double2 t) {
+          for (int e = e0; e < e1; ++e) {
+            const LvEnt E = lv.ent[e];
+            if (E.k != kk) continue;
+            if (E.tg == 0xFF) {
+              slots[(int64_t)E.slot * n * batch + bo + o] = make_double2(E.w * t.x, E.w * t.y);
+              continue;
+            }
+#pragma unroll
+            for (int q = 0; q < TGN; ++q)
+              if (E.tg == q) {
+                accs[q].x = fma(E.w, t.x, accs[q].x);
+                accs[q].y = fma(E.w, t.y, accs[q].y);
+              }
+          }
+        };
         double2 Tm[S], Tc[S], Tn[S];
 #pragma unroll
         for (int p = 0; p < S; ++p) Tm[p] = seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
-        Tk[0] = Tm[K];
+        emit(0, Tm[K]);
 #pragma unroll
         for (int k = 1; k <= K; ++k) {
           const double sc = k == 1 ? inv_L : two_L;
@@ -345,20 +375,7 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
           }
 #pragma unroll
           for (int p = 0; p < S; ++p) Tc[p] = Tn[p];
-          Tk[k] = Tc[K];
-        }
-        for (int e = lv.in_start[ii]; e < lv.in_start[ii + 1]; ++e) {
-          const LvEnt E = lv.ent[e];
-          double2 t = Tk[0];
-#pragma unroll
-          for (int k = 1; k <= K; ++k)
-            if (E.k == k) t = Tk[k];
-#pragma unroll
-          for (int q = 0; q < TGN; ++q)
-            if (E.tg == q) {
-              accs[q].x = fma(E.w, t.x, accs[q].x);
-              accs[q].y = fma(E.w, t.y, accs[q].y);
-            }
+          emit(k, Tc[K]);
         }
       }
 #pragma unroll
@@ -408,7 +425,10 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
   if (s->boxed) {
     LvAllBox axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->box(a);
-    if (lv.ntg <= 4)
+    if (lv.ntg <= 1)
+      k_level<K, 1, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv, 1.0 / L,
+                                                          2.0 / L, v, slots, y, first, osc, dotp);
+    else if (lv.ntg <= 4)
       k_level<K, 4, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv, 1.0 / L,
                                                           2.0 / L, v, slots, y, first, osc, dotp);
     else
@@ -417,7 +437,10 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
   } else {
     LvAllTab axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
-    if (lv.ntg <= 4)
+    if (lv.ntg <= 1)
+      k_level<K, 1, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv, 1.0 / L,
+                                                          2.0 / L, v, slots, y, first, osc, dotp);
+    else if (lv.ntg <= 4)
       k_level<K, 4, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv, 1.0 / L,
                                                           2.0 / L, v, slots, y, first, osc, dotp);
     else
