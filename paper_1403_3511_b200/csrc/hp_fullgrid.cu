@@ -238,16 +238,17 @@ static hp_status launch_outer(const hp_set_s* s, const double2* v, const double2
   return HP_OK;
 }
 
-// v3 pass A (compile-time ring slots): r1 <= 1
-template <int RM, int NMIX, unsigned M0, unsigned M1P, unsigned M1G>
+// v3 pass A (compile-time ring slots): r1 <= 1.  C = inner chunk; C = 2 (256-thread CTAs,
+// two per SM) measured no faster than C = 4 on cfg4 (4.90 vs 4.87 ms), so C = FG_C is used.
+template <int RM, int NMIX, unsigned M0, unsigned M1P, unsigned M1G, int C = FG_C>
 static hp_status launch_outer3(const hp_set_s* s, const double2* v, const double2* u, double2* y, const double* P,
                                const double* G, const FgPlan& F, cudaStream_t st, DotOut* dot) {
   int n0 = s->side[0], n1 = s->side[1];
-  int tile = n1 * FG_C;
-  const int64_t nblk = (int64_t)s->side[2] * s->side[3] / FG_C;
+  int tile = n1 * C;
+  const int64_t nblk = (int64_t)s->side[2] * s->side[3] / C;
   const bool use_dot = dot && dot->partial && nblk <= dot->capacity;
-  size_t smem = ((size_t)FG3_U * (n1 + 2 * FG_K) * FG_C + (size_t)FG3_NU * tile) * sizeof(double2);
-  auto kern = k_fg_outer3<RM, NMIX, M0, M1P, M1G>;
+  size_t smem = ((size_t)FG3_U * (n1 + 2 * FG_K) * C + (size_t)FG3_NU * tile) * sizeof(double2);
+  auto kern = k_fg_outer3<RM, NMIX, M0, M1P, M1G, C>;
   HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int threads = (tile + 31) / 32 * 32;
   kern<<<(unsigned)nblk, threads, smem, st>>>(v, u, y, P, P + FG_MAXN * FG_W, G, s->fg_basis, n0, n1, s->stride[0],

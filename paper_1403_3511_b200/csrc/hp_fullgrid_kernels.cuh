@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(128) k_fg_inner3(const double2* __restrict__ v
   cp_wait<0>();
 }
 
-template <int RM, int NMIX, unsigned M0, unsigned M1P, unsigned M1G>
+template <int RM, int NMIX, unsigned M0, unsigned M1P, unsigned M1G, int C = FG_C>
 __global__ void __launch_bounds__(512, 1) k_fg_outer3(const double2* __restrict__ v, const double2* __restrict__ u,
                                                       double2* __restrict__ y, const double* __restrict__ P0,
                                                       const double* __restrict__ P1, const double* __restrict__ G,
@@ -376,17 +376,17 @@ __global__ void __launch_bounds__(512, 1) k_fg_outer3(const double2* __restrict_
   static_assert(U % W == 0 && U % WS == 0 && U % WG == 0 && U % NU == 0, "unroll must cover every ring");
   static_assert(U >= K + D + 2 && NU >= D + 2, "ring too short for the prefetch distance");
   extern __shared__ double2 sm[];
-  const int tile = n1 * FG_C;
-  const int SL = (n1 + 2 * K) * FG_C;
+  const int tile = n1 * C;
+  const int SL = (n1 + 2 * K) * C;
   const int t = threadIdx.x;
   const bool act = t < tile;
-  const int j1 = t / FG_C, e = t % FG_C;
-  const int64_t off = (int64_t)j1 * S1 + (int64_t)blockIdx.x * FG_C + e;
-  double2* myring = sm + (K + j1) * FG_C + e;  // my element in ring slot 0
+  const int j1 = t / C, e = t % C;
+  const int64_t off = (int64_t)j1 * S1 + (int64_t)blockIdx.x * C + e;
+  double2* myring = sm + (K + j1) * C + e;  // my element in ring slot 0
   double2* myu = sm + U * SL + t;              // my element in u-ring slot 0
-  for (int i = t; i < U * 2 * K * FG_C; i += blockDim.x) {
-    int slot = i / (2 * K * FG_C), k = i % (2 * K * FG_C);
-    sm[slot * SL + (k < K * FG_C ? k : tile + k)] = zz();
+  for (int i = t; i < U * 2 * K * C; i += blockDim.x) {
+    int slot = i / (2 * K * C), k = i % (2 * K * C);
+    sm[slot * SL + (k < K * C ? k : tile + k)] = zz();
   }
   double p1[W], g[NM][W];
 #pragma unroll
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(512, 1) k_fg_outer3(const double2* __restrict_
     for (int d = 0; d < W; ++d) {
       constexpr unsigned any = M1P | M1G;
       if (!((any >> d) & 1)) continue;
-      double2 x = pl[(d - K) * FG_C];
+      double2 x = pl[(d - K) * C];
       if ((M1P >> d) & 1) fma2(p1[d], x, s1);
       if ((M1G >> d) & 1)
 #pragma unroll

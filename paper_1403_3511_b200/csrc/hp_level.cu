@@ -190,7 +190,8 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut)
       else if (nd.buf >= 0) released.push_back(nd.buf);
     }
     if (!B.finish()) return P;
-    if (B.L.ntg > 0) {
+    // a level whose targets are all directly written child vectors has ntg == 0 but still runs
+    if (!B.tg.empty()) {
       if (B.tg.count(BUF_Y_)) y_written = true;
       cost += B.L.nin + B.L.ntg + (B.tg.count(BUF_Y_) && P.levels.size() ? 1 : 0);
       P.levels.push_back(B.L);

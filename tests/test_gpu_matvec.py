@@ -362,3 +362,39 @@ def test_slab_shards_on_device(hp, world):
         hp.get_applier(s.set).apply_into(ap, b, yb)
         got[g.lo * g.plane:g.hi * g.plane] = yb[g.own_slice].cpu().numpy()
     assert np.array_equal(got, y_full)
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_random_term_structures_vs_oracle(hp, seed):
+    """Fuzz the evaluator planners (level-fused cuts, fused full-cube classes, trie fallback):
+    random sparse term lists on random hyperbolic / full sets, default mode vs the oracle's
+    reference-order result, real and complex, batched, with and without the oscillator."""
+    gen = np.random.default_rng(1000 + seed)
+    dim = int(gen.integers(1, 6))
+    kind = "full" if gen.random() < 0.4 else "hyperbolic"
+    if kind == "full":
+        bound = int(gen.integers(3, {1: 40, 2: 20, 3: 9, 4: 6, 5: 4}[dim]))
+        s = hp.build_full(dim, bound)
+        oa = O.applier_for_full(dim, bound)
+    else:
+        bound = int(gen.integers(2, 60))
+        s = hp.build_hyperbolic(dim, bound)
+        oa = O.applier_for_set(O.hyperbolic_indices(dim, bound))
+    nterms = int(gen.integers(1, 30))
+    maxdeg = int(gen.integers(1, 5))
+    degs = gen.integers(0, maxdeg + 1, size=(nterms, dim))
+    degs[gen.random((nterms, dim)) < 0.5] = 0
+    degs = np.unique(degs, axis=0)
+    coeffs = gen.uniform(-2, 2, degs.shape[0]) * 10.0 ** gen.uniform(-1, 2, degs.shape[0])
+    ap = _approx(degs, coeffs, dim, degree=maxdeg)
+    appl = hp.get_applier(s)
+    for cplx in (True, False):
+        v = gen.standard_normal(s.size) + (1j * gen.standard_normal(s.size) if cplx else 0.0)
+        want = oa.polynomial(degs, coeffs, 16.0, v)
+        assert rel_l2(appl.apply_polynomial(ap, v), want) < TOL, (dim, kind, bound, cplx)
+        wh = oa.hamiltonian(degs, coeffs, 16.0, v)
+        assert rel_l2(appl.apply_hamiltonian(ap, v), wh) < TOL
+    V = gen.standard_normal((3, s.size)) + 1j * gen.standard_normal((3, s.size))
+    Y = appl.apply_polynomial(ap, V)
+    for b in range(3):
+        assert rel_l2(Y[b], oa.polynomial(degs, coeffs, 16.0, V[b])) < TOL
