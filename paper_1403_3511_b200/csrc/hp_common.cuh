@@ -127,6 +127,9 @@ struct hp_set_s {
   mutable std::mutex fg_mtx;
   mutable double fg_L = 0.0;
   mutable double* fg_basis = nullptr;
+  // single-pass evaluator: blocked tile order (packed i1 | i2 << 10 | i3 << 20)
+  mutable int* fg_tiles = nullptr;
+  mutable int fg_ntiles = 0;
 
   hp::AxBox box(int a) const {
     hp::AxBox v;

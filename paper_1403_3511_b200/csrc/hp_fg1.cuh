@@ -1,0 +1,306 @@
+// Single-pass fused full-cube evaluator (cfg4 class): TMA-staged planes + register scatter ring.
+//
+// y = [c0 + sum_a P_a(X_a) + T_r0(X_0) G(X_1)] v on a 4-D box, ONE read of v and
+// ONE write of y per coefficient (32 B algorithmic), instead of the two HBM
+// passes of k_fg_inner2 / k_fg_outer3 (80 B).
+//
+// Work decomposition.  The cross-section (j1, j2, j3) is cut into 8x8x8
+// tiles; one persistent CTA per SM (512 threads, one point of the tile per
+// thread) takes tiles in a blocked order and marches axis 0 through all n0
+// planes of its tile.  For every plane p, one elected thread issues five TMA
+// boxes into a pipeline stage: the tile with its +-4 rows along j1 (axis-1
+// stencil and the G coupling), and the +-4 halos along j2 and j3.  Boxes that
+// run off the cube are zero-filled by the TMA unit, which is exactly the
+// truncation of the ladder operators at the box faces.  Halo planes of the
+// neighbouring tiles were fetched from HBM by the CTAs that own them a few
+// planes earlier (all 148 CTAs march at the same rate over a compact block
+// of tiles), so they come from L2.
+//
+// Axis 0 is the march axis: instead of a 9-plane window of v, each thread
+// keeps a 9-slot ring of PARTIAL OUTPUTS y(p-4 .. p+4) in registers.  When
+// plane p arrives it scatters c = v(p) into y(p + d) with the band weight
+// P_0(p + d, -d) (uniform over the CTA), adds the in-plane stencil of axes
+// 1-3 and scatters g = G v(p) through T_r0(X_0); y(p-4) is then complete and
+// is stored.  Ring slots are compile-time (march unrolled by 9).
+//
+// Weights: the in-plane band rows of the thread's (j1, j2, j3) are loaded once
+// per tile into registers; the axis-0 rows are broadcast loads per plane.
+#pragma once
+
+#include <cuda.h>
+
+namespace hp {
+
+constexpr int F1_T = 8;                 // tile edge along axes 1, 2, 3
+constexpr int F1_H = FG_K;              // halo (band radius)
+constexpr int F1_S = 6;                 // pipeline stages
+constexpr int F1_THREADS = F1_T * F1_T * F1_T;
+// stage layout in double2 units: [j1 +-4][j2][j3] | j3 halos lo, hi | j2 halos lo, hi
+constexpr int F1_A1 = (F1_T + 2 * F1_H) * F1_T * F1_T;  // 1024
+constexpr int F1_A3 = F1_T * F1_T * F1_H;               // 256  ([j1][j2][4])
+constexpr int F1_B2 = F1_T * F1_H * F1_T;               // 256  ([j1][4][j3])
+constexpr int F1_OFF_A3LO = F1_A1;
+constexpr int F1_OFF_A3HI = F1_A1 + F1_A3;
+constexpr int F1_OFF_B2LO = F1_A1 + 2 * F1_A3;
+constexpr int F1_OFF_B2HI = F1_A1 + 2 * F1_A3 + F1_B2;
+constexpr int F1_STAGE = F1_A1 + 2 * F1_A3 + 2 * F1_B2;  // 2048 double2 = 32 KB
+constexpr unsigned F1_STAGE_BYTES = F1_STAGE * 16u;
+constexpr int F1_WROW = 8;  // per-plane scatter weights (doubles), see k_fg_single
+constexpr size_t F1_WOFF = (size_t)F1_S * F1_STAGE_BYTES;
+constexpr size_t F1_BOFF = F1_WOFF + (size_t)FG_MAXN * F1_WROW * sizeof(double);
+constexpr size_t F1_SMEM = F1_BOFF + 2 * F1_S * sizeof(uint64_t) + 8 * sizeof(int);
+
+__device__ __forceinline__ unsigned f1_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void f1_mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(f1_saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void f1_mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(f1_saddr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void f1_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(f1_saddr(bar)) : "memory");
+}
+__device__ __forceinline__ bool f1_mbar_try(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(ok)
+      : "r"(f1_saddr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// bounded wait: a TMA that never lands traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void f1_mbar_wait(uint64_t* bar, unsigned parity) {
+  if (f1_mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!f1_mbar_try(bar, parity))
+    if (clock64() - t0 > (1ll << 33)) __trap();
+}
+__device__ __forceinline__ void f1_tma4(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
+                                        uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];\n" ::"r"(f1_saddr(dst)),
+      "l"((unsigned long long)m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(f1_saddr(bar))
+      : "memory");
+}
+
+
+// NMIX = 0: no coupling term; NMIX = 1: one T_1(X_0) G(X_1) class with G on diagonals +-1.
+// Single-axis bands on all four axes are even (diagonals 0, +-2, +-4).
+//
+// Pipeline: thread 0 is the producer.  Stage s carries a "full" mbarrier (TMA
+// transaction bytes) and an "empty" mbarrier (one arrival per warp once the
+// warp has read the stage); the producer refills a stage only after its empty
+// phase completes, so warps drift freely up to F1_S - 2 planes apart.
+template <int NMIX, bool DOT>
+__global__ void __launch_bounds__(F1_THREADS, 1)
+    k_fg_single(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mA3,
+                const __grid_constant__ CUtensorMap mB2, const double2* __restrict__ v, double2* __restrict__ y,
+                const double* __restrict__ P, const double* __restrict__ G, const double* __restrict__ B0,
+                const int* __restrict__ tiles, int ntiles, int n0, int n1, int n2, int n3,
+                double2* __restrict__ dotp) {
+  extern __shared__ __align__(128) unsigned char f1_smem[];
+  double2* stg = (double2*)f1_smem;
+  double* W = (double*)(f1_smem + F1_WOFF);
+  uint64_t* full = (uint64_t*)(f1_smem + F1_BOFF);
+  uint64_t* empty = full + F1_S;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int j3 = tid & 7, j2 = (tid >> 3) & 7, j1 = tid >> 6;
+  const double* P0 = P;
+  const double* P1 = P + FG_MAXN * FG_W;
+  const double* P2 = P + 2 * FG_MAXN * FG_W;
+  const double* P3 = P + 3 * FG_MAXN * FG_W;
+  if (tid == 0) {
+    for (int s = 0; s < F1_S; ++s) {
+      f1_mbar_init(&full[s], 1);
+      f1_mbar_init(&empty[s], F1_THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // per-plane scatter weights: row p = {P0(p,0), P0(p+2,-2), P0(p-2,2), P0(p+4,-4), P0(p-4,4),
+  //                                     B0(p+1,-1), B0(p-1,1), 0}
+  for (int q = tid; q < n0; q += F1_THREADS) {
+    auto p0 = [&](int r, int e) { return (r >= 0 && r < n0) ? P0[r * FG_W + e + FG_K] : 0.0; };
+    auto b0 = [&](int r, int e) { return (NMIX && r >= 0 && r < n0) ? B0[r * FG_W + e + FG_K] : 0.0; };
+    double* w = W + q * F1_WROW;
+    w[0] = p0(q, 0);
+    w[1] = p0(q + 2, -2);
+    w[2] = p0(q - 2, 2);
+    w[3] = p0(q + 4, -4);
+    w[4] = p0(q - 4, 4);
+    w[5] = b0(q + 1, -1);
+    w[6] = b0(q - 1, 1);
+    w[7] = 0.0;
+  }
+  __syncthreads();
+
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nitems = my_tiles * n0;
+  // producer state (thread 0 only; kept in shared memory so that it costs the
+  // consumer threads no registers): next item, its tile / plane / stage / stage-use
+  // count and the tile origin
+  int* ps_ = (int*)(empty + F1_S);
+  if (tid == 0)
+    for (int i = 0; i < 8; ++i) ps_[i] = 0;
+  auto issue_next = [&]() {
+    int pk = ps_[0], pti = ps_[1], pp = ps_[2], ps = ps_[3], pu = ps_[4];
+    if (pk >= nitems) return;
+    if (pu > 0) f1_mbar_wait(&empty[ps], (unsigned)((pu - 1) & 1));
+    if (pp == 0) {
+      const int code = __ldg(tiles + blockIdx.x + pti * gridDim.x);
+      ps_[5] = (code & 1023) * F1_T;
+      ps_[6] = ((code >> 10) & 1023) * F1_T;
+      ps_[7] = (code >> 20) * F1_T;
+    }
+    const int T1 = ps_[5], T2 = ps_[6], T3 = ps_[7];
+    double2* dst = stg + (size_t)ps * F1_STAGE;
+    uint64_t* bar = &full[ps];
+    f1_mbar_expect(bar, F1_STAGE_BYTES);
+    f1_tma4(dst, &mA1, 2 * T3, T2, T1 - F1_H, pp, bar);
+    f1_tma4(dst + F1_OFF_A3LO, &mA3, 2 * (T3 - F1_H), T2, T1, pp, bar);
+    f1_tma4(dst + F1_OFF_A3HI, &mA3, 2 * (T3 + F1_T), T2, T1, pp, bar);
+    f1_tma4(dst + F1_OFF_B2LO, &mB2, 2 * T3, T2 - F1_H, T1, pp, bar);
+    f1_tma4(dst + F1_OFF_B2HI, &mB2, 2 * T3, T2 + F1_T, T1, pp, bar);
+    ++pk;
+    if (++pp == n0) {
+      pp = 0;
+      ++pti;
+    }
+    if (++ps == F1_S) {
+      ps = 0;
+      ++pu;
+    }
+    ps_[0] = pk;
+    ps_[1] = pti;
+    ps_[2] = pp;
+    ps_[3] = ps;
+    ps_[4] = pu;
+  };
+  if (tid == 0)
+    for (int k = 0; k < F1_S - 1; ++k) issue_next();
+
+  // stage-relative offsets of this thread's taps (double2 units)
+  const int oc = (j1 + F1_H) * 64 + j2 * 8 + j3;
+  // halo taps (j2 or j3 outside the tile) live in the side boxes; computed on the fly
+  // (cheap integer selects) so that they do not hold registers across the march
+  auto o2 = [&](int d) {
+    const int a = j2 + d;
+    return a < 0 ? F1_OFF_B2LO + j1 * 32 + (a + F1_H) * 8 + j3
+                 : (a >= F1_T ? F1_OFF_B2HI + j1 * 32 + (a - F1_T) * 8 + j3 : oc + d * 8);
+  };
+  auto o3 = [&](int d) {
+    const int b = j3 + d;
+    return b < 0 ? F1_OFF_A3LO + j1 * 32 + j2 * 4 + (b + F1_H)
+                 : (b >= F1_T ? F1_OFF_A3HI + j1 * 32 + j2 * 4 + (b - F1_T) : oc + d);
+  };
+
+  double2 dacc = make_double2(0.0, 0.0);
+  int cs = 0, cu = 0;  // consumer stage / stage-use count
+  const int64_t plane = (int64_t)n1 * n2 * n3;
+  for (int ti = 0; ti < my_tiles; ++ti) {
+    const int code = __ldg(tiles + blockIdx.x + ti * gridDim.x);
+    const int J1 = (code & 1023) * F1_T + j1, J2 = ((code >> 10) & 1023) * F1_T + j2,
+              J3 = (code >> 20) * F1_T + j3;
+    const bool inside = J1 < n1 && J2 < n2 && J3 < n3;
+    const int c1 = min(J1, FG_MAXN - 1), c2 = min(J2, FG_MAXN - 1), c3 = min(J3, FG_MAXN - 1);
+    double w1[4], w2[4], w3[4], wg0 = 0.0, wg1 = 0.0;
+    {
+      const int ds[4] = {-4, -2, 2, 4};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        w1[i] = __ldg(P1 + c1 * FG_W + ds[i] + FG_K);
+        w2[i] = __ldg(P2 + c2 * FG_W + ds[i] + FG_K);
+        w3[i] = __ldg(P3 + c3 * FG_W + ds[i] + FG_K);
+      }
+      if (NMIX) {
+        wg0 = __ldg(G + c1 * FG_W + FG_K - 1);
+        wg1 = __ldg(G + c1 * FG_W + FG_K + 1);
+      }
+    }
+    const double cc = __ldg(P1 + c1 * FG_W + FG_K) + __ldg(P2 + c2 * FG_W + FG_K) + __ldg(P3 + c3 * FG_W + FG_K);
+    const int col = (J1 * n2 + J2) * n3 + J3;  // n1 n2 n3 <= 2^24
+
+    double2 R[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = make_double2(0.0, 0.0);
+
+    for (int pb = 0; pb < n0 + F1_H; pb += 9) {
+      unroll<9>([&](auto UU) {
+        constexpr int U = decltype(UU)::value;
+        const int p = pb + U;
+        if (p >= n0 + F1_H) return;
+        if (p < n0) {
+          if (tid == 0) issue_next();
+          f1_mbar_wait(&full[cs], (unsigned)(cu & 1));
+          const double2* st = stg + (size_t)cs * F1_STAGE;
+          // three load groups separated by compiler fences: bounds the registers held by
+          // in-flight shared loads (ring + weights already take ~70)
+          const double2 c = st[oc];
+          const double2 a1m4 = st[oc - 256], a1m2 = st[oc - 128], a1p2 = st[oc + 128], a1p4 = st[oc + 256];
+          double2 gm, gp;
+          if (NMIX) {
+            gm = st[oc - 64];
+            gp = st[oc + 64];
+          }
+          double2 u = make_double2(cc * c.x, cc * c.y);
+          fma2(w1[0], a1m4, u);
+          fma2(w1[1], a1m2, u);
+          fma2(w1[2], a1p2, u);
+          fma2(w1[3], a1p4, u);
+          asm volatile("" ::: "memory");
+          const double2 a2m4 = st[o2(-4)], a2m2 = st[o2(-2)], a2p2 = st[o2(2)], a2p4 = st[o2(4)];
+          fma2(w2[0], a2m4, u);
+          fma2(w2[1], a2m2, u);
+          fma2(w2[2], a2p2, u);
+          fma2(w2[3], a2p4, u);
+          asm volatile("" ::: "memory");
+          const double2 a3m4 = st[o3(-4)], a3m2 = st[o3(-2)], a3p2 = st[o3(2)], a3p4 = st[o3(4)];
+          fma2(w3[0], a3m4, u);
+          fma2(w3[1], a3m2, u);
+          fma2(w3[2], a3p2, u);
+          fma2(w3[3], a3p4, u);
+          __syncwarp();
+          if (lane == 0) f1_mbar_arrive(&empty[cs]);
+          if (++cs == F1_S) {
+            cs = 0;
+            ++cu;
+          }
+          const double2 wa = *(const double2*)(W + p * F1_WROW);
+          const double2 wb = *(const double2*)(W + p * F1_WROW + 2);
+          const double2 wc = *(const double2*)(W + p * F1_WROW + 4);
+          const double2 wd = *(const double2*)(W + p * F1_WROW + 6);
+          fma2(wa.x, c, u);
+          R[U].x += u.x;
+          R[U].y += u.y;
+          fma2(wa.y, c, R[(U + 2) % 9]);
+          fma2(wb.x, c, R[(U + 7) % 9]);
+          fma2(wb.y, c, R[(U + 4) % 9]);
+          fma2(wc.x, c, R[(U + 5) % 9]);
+          if (NMIX) {
+            double2 g = make_double2(wg0 * gm.x, wg0 * gm.y);
+            fma2(wg1, gp, g);
+            fma2(wc.y, g, R[(U + 1) % 9]);
+            fma2(wd.x, g, R[(U + 8) % 9]);
+          }
+        }
+        // y(p - 4) has received its last contribution
+        constexpr int SQ = (U + 5) % 9;
+        if (p >= F1_H && inside) {
+          const int64_t gi = (int64_t)(p - F1_H) * plane + col;
+          y[gi] = R[SQ];
+          if (DOT) cdot_acc(__ldg(v + gi), R[SQ], dacc);
+        }
+        R[SQ] = make_double2(0.0, 0.0);
+      });
+    }
+  }
+  if (DOT) {
+    dacc = block_sum2(dacc);
+    if (tid == 0) dotp[blockIdx.x] = dacc;
+  }
+}
+
+}  // namespace hp

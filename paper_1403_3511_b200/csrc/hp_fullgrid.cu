@@ -202,8 +202,102 @@ __global__ void k_fg_combine(const double* __restrict__ basis, double* __restric
 }  // namespace hp
 
 #include "hp_fullgrid_kernels.cuh"
+#include "hp_fg1.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace hp {
+
+// ---------------------------------------------------------------- single pass (TMA)
+
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }();
+  return fn;
+}
+
+// 4-D map over a complex box viewed as f64 [n0][n1][n2][2 n3]; box (b0 doubles, b1, b2, 1)
+static bool tma_map(CUtensorMap* m, const void* base, const int side[4], unsigned b0, unsigned b1, unsigned b2) {
+  auto enc = tma_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {2ull * side[3], (cuuint64_t)side[2], (cuuint64_t)side[1], (cuuint64_t)side[0]};
+  cuuint64_t strides[3] = {16ull * side[3], 16ull * side[2] * side[3], 16ull * side[1] * side[2] * side[3]};
+  cuuint32_t box[4] = {b0, b1, b2, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// tile order: 3x3 blocks of (i1, i2) columns, i3 fastest, so that the ~148 tiles in
+// flight form a compact block whose halos are shared through L2
+static hp_status ensure_tiles(const hp_set_s* s) {
+  std::lock_guard<std::mutex> g(s->fg_mtx);
+  if (s->fg_tiles) return HP_OK;
+  const int t1 = (s->side[1] + F1_T - 1) / F1_T, t2 = (s->side[2] + F1_T - 1) / F1_T,
+            t3 = (s->side[3] + F1_T - 1) / F1_T;
+  constexpr int BE = 3;
+  std::vector<int> codes;
+  codes.reserve((size_t)t1 * t2 * t3);
+  for (int b1 = 0; b1 < t1; b1 += BE)
+    for (int b2 = 0; b2 < t2; b2 += BE)
+      for (int i1 = b1; i1 < std::min(t1, b1 + BE); ++i1)
+        for (int i2 = b2; i2 < std::min(t2, b2 + BE); ++i2)
+          for (int i3 = 0; i3 < t3; ++i3) codes.push_back(i1 | (i2 << 10) | (i3 << 20));
+  int* d = nullptr;
+  HP_CUDA(cudaMalloc(&d, codes.size() * sizeof(int)));
+  HP_CUDA(cudaMemcpy(d, codes.data(), codes.size() * sizeof(int), cudaMemcpyHostToDevice));
+  s->fg_ntiles = (int)codes.size();
+  s->fg_tiles = d;
+  return HP_OK;
+}
+
+static bool fg_single_enabled() {
+  static int v = [] {
+    const char* e = getenv("HP_FG_SINGLE");
+    return e && atoi(e) == 0 ? 0 : 1;
+  }();
+  return v == 1;
+}
+
+static int sm_count() {
+  static int n = [] {
+    int dev = 0, c = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    return c;
+  }();
+  return n;
+}
+
+template <int NMIX>
+static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, const double* P, const double* G,
+                               const FgPlan& F, cudaStream_t st, DotOut* dot, bool* launched) {
+  *launched = false;
+  CUtensorMap mA1, mA3, mB2;
+  if (!tma_map(&mA1, v, s->side, 2 * F1_T, F1_T, F1_T + 2 * F1_H) ||
+      !tma_map(&mA3, v, s->side, 2 * F1_H, F1_T, F1_T) || !tma_map(&mB2, v, s->side, 2 * F1_T, F1_H, F1_T))
+    return HP_OK;  // no driver entry point: the two-pass kernels run
+  hp_status rc = ensure_tiles(s);
+  if (rc) return rc;
+  const int n0 = s->side[0];
+  const double* B0 = s->fg_basis + (size_t)(NMIX ? F.r0[0] : 0) * n0 * FG_W;  // axis 0, degree r0
+  const int grid = std::min(s->fg_ntiles, sm_count());
+  const bool use_dot = dot && dot->partial && grid <= dot->capacity;
+  auto kern = use_dot ? k_fg_single<NMIX, true> : k_fg_single<NMIX, false>;
+  HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F1_SMEM));
+  kern<<<grid, F1_THREADS, F1_SMEM, st>>>(mA1, mA3, mB2, v, y, P, G, B0, s->fg_tiles, s->fg_ntiles, n0,
+                                          s->side[1], s->side[2], s->side[3], use_dot ? dot->partial : nullptr);
+  HP_LAUNCH_CHECK("k_fg_single");
+  if (use_dot) dot->n = grid;
+  *launched = true;
+  return HP_OK;
+}
 
 template <unsigned M2, unsigned M3>
 static hp_status launch_inner(const hp_set_s* s, const double2* v, double2* u, const double* P, cudaStream_t st) {
@@ -295,6 +389,18 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   const double2* v = (const double2*)in;
   double2* y = (double2*)out;
   const bool even = F.mask[0] == FG_MASK_EVEN && F.mask[2] == FG_MASK_EVEN && F.mask[3] == FG_MASK_EVEN;
+  // single pass for the even-band class (cfg4)
+  if (fg_single_enabled() && even && F.mask[1] == FG_MASK_EVEN &&
+      (F.nmix == 0 || (F.nmix == 1 && F.rm == 1 && (F.maskG & ~FG_MASK_PM1) == 0))) {
+    bool launched = false;
+    rc = F.nmix ? launch_single<1>(s, v, y, P, G, F, st, dot, &launched)
+                : launch_single<0>(s, v, y, P, G, F, st, dot, &launched);
+    if (rc) return rc;
+    if (launched) {
+      *done = true;
+      return HP_OK;
+    }
+  }
   // pass B
   rc = even ? launch_inner<FG_MASK_EVEN, FG_MASK_EVEN>(s, v, u, P, st)
             : launch_inner<FG_MASK_ALL, FG_MASK_ALL>(s, v, u, P, st);

@@ -499,6 +499,7 @@ hp_status hp_set_destroy(hp_set_t s) {
   if (s->d_pref) cudaFree(s->d_pref);
   if (s->d_off) cudaFree(s->d_off);
   if (s->fg_basis) cudaFree(s->fg_basis);
+  if (s->fg_tiles) cudaFree(s->fg_tiles);
   delete s;
   return HP_OK;
 }
