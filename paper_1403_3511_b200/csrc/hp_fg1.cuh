@@ -33,17 +33,16 @@ namespace hp {
 
 constexpr int F1_T = 8;                 // tile edge along axes 1, 2, 3
 constexpr int F1_H = FG_K;              // halo (band radius)
-constexpr int F1_S = 6;                 // pipeline stages
-constexpr int F1_THREADS = F1_T * F1_T * F1_T;
-// stage layout in double2 units: [j1 +-4][j2][j3] | j3 halos lo, hi | j2 halos lo, hi
-constexpr int F1_A1 = (F1_T + 2 * F1_H) * F1_T * F1_T;  // 1024
-constexpr int F1_A3 = F1_T * F1_T * F1_H;               // 256  ([j1][j2][4])
-constexpr int F1_B2 = F1_T * F1_H * F1_T;               // 256  ([j1][4][j3])
-constexpr int F1_OFF_A3LO = F1_A1;
-constexpr int F1_OFF_A3HI = F1_A1 + F1_A3;
-constexpr int F1_OFF_B2LO = F1_A1 + 2 * F1_A3;
-constexpr int F1_OFF_B2HI = F1_A1 + 2 * F1_A3 + F1_B2;
-constexpr int F1_STAGE = F1_A1 + 2 * F1_A3 + 2 * F1_B2;  // 2048 double2 = 32 KB
+constexpr int F1_S = 5;                 // pipeline stages
+constexpr int F1_POINTS = F1_T * F1_T * F1_T;  // tile points (512)
+// stage layout in double2 units: A1 = [j1 +-4][j2][j3 +-4] (256 B rows: the j3 halos ride in the
+// tile rows -- 64 B halo rows cost the TMA unit twice as much per byte) | j2 halos lo, hi
+constexpr int F1_RW = F1_T + 2 * F1_H;                   // A1 row (j3) length
+constexpr int F1_A1 = (F1_T + 2 * F1_H) * F1_T * F1_RW;  // 2048
+constexpr int F1_B2 = F1_T * F1_H * F1_T;                // 256  ([j1][4][j3])
+constexpr int F1_OFF_B2LO = F1_A1;
+constexpr int F1_OFF_B2HI = F1_A1 + F1_B2;
+constexpr int F1_STAGE = F1_A1 + 2 * F1_B2;  // 2560 double2 = 40 KB
 constexpr unsigned F1_STAGE_BYTES = F1_STAGE * 16u;
 constexpr int F1_WROW = 8;  // per-plane scatter weights (doubles), see k_fg_single
 constexpr size_t F1_WOFF = (size_t)F1_S * F1_STAGE_BYTES;
@@ -91,24 +90,30 @@ __device__ __forceinline__ void f1_tma4(void* dst, const CUtensorMap* m, int c0,
 // NMIX = 0: no coupling term; NMIX = 1: one T_1(X_0) G(X_1) class with G on diagonals +-1.
 // Single-axis bands on all four axes are even (diagonals 0, +-2, +-4).
 //
+// NP points per thread (512 / NP threads): with NP = 2 a thread owns tile rows j1 and j1 + 2
+// (rows {0,2}, {1,3}, {4,6}, {5,7}), whose axis-1 and G taps overlap: 9 shared-memory loads
+// serve both points' axis-1 + coupling + centre terms instead of 14, which is what bounds
+// this kernel (the shared-memory pipe), at the price of a second register ring.
+//
 // Pipeline: thread 0 is the producer.  Stage s carries a "full" mbarrier (TMA
 // transaction bytes) and an "empty" mbarrier (one arrival per warp once the
 // warp has read the stage); the producer refills a stage only after its empty
 // phase completes, so warps drift freely up to F1_S - 2 planes apart.
-template <int NMIX, bool DOT>
-__global__ void __launch_bounds__(F1_THREADS, 1)
-    k_fg_single(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mA3,
-                const __grid_constant__ CUtensorMap mB2, const double2* __restrict__ v, double2* __restrict__ y,
-                const double* __restrict__ P, const double* __restrict__ G, const double* __restrict__ B0,
-                const int* __restrict__ tiles, int ntiles, int n0, int n1, int n2, int n3,
-                double2* __restrict__ dotp) {
+template <int NMIX, bool DOT, int NP>
+__global__ void __launch_bounds__(F1_POINTS / NP, 1)
+    k_fg_single(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB2,
+                const double2* __restrict__ v, double2* __restrict__ y, const double* __restrict__ P,
+                const double* __restrict__ G, const double* __restrict__ B0, const int* __restrict__ tiles,
+                int ntiles, int n0, int n1, int n2, int n3, double2* __restrict__ dotp, int exp) {
+  constexpr int NT = F1_POINTS / NP;
   extern __shared__ __align__(128) unsigned char f1_smem[];
   double2* stg = (double2*)f1_smem;
   double* W = (double*)(f1_smem + F1_WOFF);
   uint64_t* full = (uint64_t*)(f1_smem + F1_BOFF);
   uint64_t* empty = full + F1_S;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int j3 = tid & 7, j2 = (tid >> 3) & 7, j1 = tid >> 6;
+  const int j3 = tid & 7, j2 = (tid >> 3) & 7;
+  const int j1 = NP == 1 ? (tid >> 6) : (((tid >> 6) >> 1) * 4 + ((tid >> 6) & 1));  // first row
   const double* P0 = P;
   const double* P1 = P + FG_MAXN * FG_W;
   const double* P2 = P + 2 * FG_MAXN * FG_W;
@@ -116,13 +121,13 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
   if (tid == 0) {
     for (int s = 0; s < F1_S; ++s) {
       f1_mbar_init(&full[s], 1);
-      f1_mbar_init(&empty[s], F1_THREADS / 32);
+      f1_mbar_init(&empty[s], NT / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // per-plane scatter weights: row p = {P0(p,0), P0(p+2,-2), P0(p-2,2), P0(p+4,-4), P0(p-4,4),
   //                                     B0(p+1,-1), B0(p-1,1), 0}
-  for (int q = tid; q < n0; q += F1_THREADS) {
+  for (int q = tid; q < n0; q += NT) {
     auto p0 = [&](int r, int e) { return (r >= 0 && r < n0) ? P0[r * FG_W + e + FG_K] : 0.0; };
     auto b0 = [&](int r, int e) { return (NMIX && r >= 0 && r < n0) ? B0[r * FG_W + e + FG_K] : 0.0; };
     double* w = W + q * F1_WROW;
@@ -139,9 +144,8 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
 
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int nitems = my_tiles * n0;
-  // producer state (thread 0 only; kept in shared memory so that it costs the
-  // consumer threads no registers): next item, its tile / plane / stage / stage-use
-  // count and the tile origin
+  // producer state (thread 0 only; kept in shared memory so that it costs the consumer
+  // threads no registers): next item, its tile / plane / stage / stage-use count, tile origin
   int* ps_ = (int*)(empty + F1_S);
   if (tid == 0)
     for (int i = 0; i < 8; ++i) ps_[i] = 0;
@@ -158,12 +162,12 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
     const int T1 = ps_[5], T2 = ps_[6], T3 = ps_[7];
     double2* dst = stg + (size_t)ps * F1_STAGE;
     uint64_t* bar = &full[ps];
-    f1_mbar_expect(bar, F1_STAGE_BYTES);
-    f1_tma4(dst, &mA1, 2 * T3, T2, T1 - F1_H, pp, bar);
-    f1_tma4(dst + F1_OFF_A3LO, &mA3, 2 * (T3 - F1_H), T2, T1, pp, bar);
-    f1_tma4(dst + F1_OFF_A3HI, &mA3, 2 * (T3 + F1_T), T2, T1, pp, bar);
-    f1_tma4(dst + F1_OFF_B2LO, &mB2, 2 * T3, T2 - F1_H, T1, pp, bar);
-    f1_tma4(dst + F1_OFF_B2HI, &mB2, 2 * T3, T2 + F1_T, T1, pp, bar);
+    f1_mbar_expect(bar, (exp & 1) ? F1_A1 * 16u : F1_STAGE_BYTES);
+    f1_tma4(dst, &mA1, 2 * (T3 - F1_H), T2, T1 - F1_H, pp, bar);
+    if (!(exp & 1)) {
+      f1_tma4(dst + F1_OFF_B2LO, &mB2, 2 * T3, T2 - F1_H, T1, pp, bar);
+      f1_tma4(dst + F1_OFF_B2HI, &mB2, 2 * T3, T2 + F1_T, T1, pp, bar);
+    }
     ++pk;
     if (++pp == n0) {
       pp = 0;
@@ -182,19 +186,16 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
   if (tid == 0)
     for (int k = 0; k < F1_S - 1; ++k) issue_next();
 
-  // stage-relative offsets of this thread's taps (double2 units)
-  const int oc = (j1 + F1_H) * 64 + j2 * 8 + j3;
-  // halo taps (j2 or j3 outside the tile) live in the side boxes; computed on the fly
-  // (cheap integer selects) so that they do not hold registers across the march
-  auto o2 = [&](int d) {
+  constexpr int R1 = F1_T * F1_RW;  // A1 j1-row stride (double2)
+  // centre of point 0 in A1; point 1 (NP = 2) sits two j1 rows below
+  const int oc = (j1 + F1_H) * R1 + j2 * F1_RW + j3 + F1_H;
+  // axis-2 taps: inside the tile they are A1 rows, outside they live in the j2 halo boxes
+  // (computed on the fly so they hold no registers across the march)
+  auto o2 = [&](int row, int d) {
     const int a = j2 + d;
-    return a < 0 ? F1_OFF_B2LO + j1 * 32 + (a + F1_H) * 8 + j3
-                 : (a >= F1_T ? F1_OFF_B2HI + j1 * 32 + (a - F1_T) * 8 + j3 : oc + d * 8);
-  };
-  auto o3 = [&](int d) {
-    const int b = j3 + d;
-    return b < 0 ? F1_OFF_A3LO + j1 * 32 + j2 * 4 + (b + F1_H)
-                 : (b >= F1_T ? F1_OFF_A3HI + j1 * 32 + j2 * 4 + (b - F1_T) : oc + d);
+    return a < 0 ? F1_OFF_B2LO + row * 32 + (a + F1_H) * 8 + j3
+                 : (a >= F1_T ? F1_OFF_B2HI + row * 32 + (a - F1_T) * 8 + j3
+                              : (row + F1_H) * R1 + a * F1_RW + j3 + F1_H);
   };
 
   double2 dacc = make_double2(0.0, 0.0);
@@ -204,28 +205,41 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
     const int code = __ldg(tiles + blockIdx.x + ti * gridDim.x);
     const int J1 = (code & 1023) * F1_T + j1, J2 = ((code >> 10) & 1023) * F1_T + j2,
               J3 = (code >> 20) * F1_T + j3;
-    const bool inside = J1 < n1 && J2 < n2 && J3 < n3;
-    const int c1 = min(J1, FG_MAXN - 1), c2 = min(J2, FG_MAXN - 1), c3 = min(J3, FG_MAXN - 1);
-    double w1[4], w2[4], w3[4], wg0 = 0.0, wg1 = 0.0;
+    const bool in0 = J1 < n1 && J2 < n2 && J3 < n3;
+    const bool in1 = NP == 2 && J1 + 2 < n1 && J2 < n2 && J3 < n3;
+    const int c1a = min(J1, FG_MAXN - 1), c1b = min(J1 + 2, FG_MAXN - 1);
+    const int c2 = min(J2, FG_MAXN - 1), c3 = min(J3, FG_MAXN - 1);
+    double w1a[4], w1b[4], w2[4], w3[4];
+    double wga0 = 0.0, wga1 = 0.0, wgb0 = 0.0, wgb1 = 0.0;
     {
       const int ds[4] = {-4, -2, 2, 4};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        w1[i] = __ldg(P1 + c1 * FG_W + ds[i] + FG_K);
+        w1a[i] = __ldg(P1 + c1a * FG_W + ds[i] + FG_K);
+        w1b[i] = NP == 2 ? __ldg(P1 + c1b * FG_W + ds[i] + FG_K) : 0.0;
         w2[i] = __ldg(P2 + c2 * FG_W + ds[i] + FG_K);
         w3[i] = __ldg(P3 + c3 * FG_W + ds[i] + FG_K);
       }
       if (NMIX) {
-        wg0 = __ldg(G + c1 * FG_W + FG_K - 1);
-        wg1 = __ldg(G + c1 * FG_W + FG_K + 1);
+        wga0 = __ldg(G + c1a * FG_W + FG_K - 1);
+        wga1 = __ldg(G + c1a * FG_W + FG_K + 1);
+        if (NP == 2) {
+          wgb0 = __ldg(G + c1b * FG_W + FG_K - 1);
+          wgb1 = __ldg(G + c1b * FG_W + FG_K + 1);
+        }
       }
     }
-    const double cc = __ldg(P1 + c1 * FG_W + FG_K) + __ldg(P2 + c2 * FG_W + FG_K) + __ldg(P3 + c3 * FG_W + FG_K);
+    const double c23 = __ldg(P2 + c2 * FG_W + FG_K) + __ldg(P3 + c3 * FG_W + FG_K);
+    const double cca = __ldg(P1 + c1a * FG_W + FG_K) + c23;
+    const double ccb = NP == 2 ? __ldg(P1 + c1b * FG_W + FG_K) + c23 : 0.0;
     const int col = (J1 * n2 + J2) * n3 + J3;  // n1 n2 n3 <= 2^24
+    const int colb = col + 2 * n2 * n3;
 
-    double2 R[9];
+    double2 RA[9], RB[NP == 2 ? 9 : 1];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) R[i] = make_double2(0.0, 0.0);
+    for (int i = 0; i < 9; ++i) RA[i] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < (NP == 2 ? 9 : 1); ++i) RB[i] = make_double2(0.0, 0.0);
 
     for (int pb = 0; pb < n0 + F1_H; pb += 9) {
       unroll<9>([&](auto UU) {
@@ -235,33 +249,86 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
         if (p < n0) {
           if (tid == 0) issue_next();
           f1_mbar_wait(&full[cs], (unsigned)(cu & 1));
-          const double2* st = stg + (size_t)cs * F1_STAGE;
-          // three load groups separated by compiler fences: bounds the registers held by
-          // in-flight shared loads (ring + weights already take ~70)
-          const double2 c = st[oc];
-          const double2 a1m4 = st[oc - 256], a1m2 = st[oc - 128], a1p2 = st[oc + 128], a1p4 = st[oc + 256];
-          double2 gm, gp;
-          if (NMIX) {
-            gm = st[oc - 64];
-            gp = st[oc + 64];
+          if (exp & 2) {  // timing experiment: pipeline only
+            __syncwarp();
+            if (lane == 0) f1_mbar_arrive(&empty[cs]);
+            if (++cs == F1_S) {
+              cs = 0;
+              ++cu;
+            }
+            return;
           }
-          double2 u = make_double2(cc * c.x, cc * c.y);
-          fma2(w1[0], a1m4, u);
-          fma2(w1[1], a1m2, u);
-          fma2(w1[2], a1p2, u);
-          fma2(w1[3], a1p4, u);
+          const double2* st = stg + (size_t)cs * F1_STAGE;
+          // load groups separated by compiler fences: bounds the registers held by in-flight
+          // shared loads (rings + weights already take most of the budget)
+          double2 ua, ub = make_double2(0.0, 0.0), ga = make_double2(0.0, 0.0), gb = make_double2(0.0, 0.0);
+          double2 ca, cb = make_double2(0.0, 0.0);
+          {
+            const double2 m4 = st[oc - 4 * R1], m2 = st[oc - 2 * R1], z0 = st[oc], p2 = st[oc + 2 * R1],
+                          p4 = st[oc + 4 * R1];
+            ca = z0;
+            ua = make_double2(cca * z0.x, cca * z0.y);
+            fma2(w1a[0], m4, ua);
+            fma2(w1a[1], m2, ua);
+            fma2(w1a[2], p2, ua);
+            fma2(w1a[3], p4, ua);
+            if (NP == 2) {
+              const double2 p6 = st[oc + 6 * R1];
+              cb = p2;
+              ub = make_double2(ccb * p2.x, ccb * p2.y);
+              fma2(w1b[0], m2, ub);
+              fma2(w1b[1], z0, ub);
+              fma2(w1b[2], p4, ub);
+              fma2(w1b[3], p6, ub);
+            }
+          }
+          if (NMIX) {
+            asm volatile("" ::: "memory");
+            const double2 m1 = st[oc - R1], p1 = st[oc + R1];
+            ga = make_double2(wga0 * m1.x, wga0 * m1.y);
+            fma2(wga1, p1, ga);
+            if (NP == 2) {
+              const double2 p3 = st[oc + 3 * R1];
+              gb = make_double2(wgb0 * p1.x, wgb0 * p1.y);
+              fma2(wgb1, p3, gb);
+            }
+          }
           asm volatile("" ::: "memory");
-          const double2 a2m4 = st[o2(-4)], a2m2 = st[o2(-2)], a2p2 = st[o2(2)], a2p4 = st[o2(4)];
-          fma2(w2[0], a2m4, u);
-          fma2(w2[1], a2m2, u);
-          fma2(w2[2], a2p2, u);
-          fma2(w2[3], a2p4, u);
+          {
+            const double2 a = st[o2(j1, -4)], b = st[o2(j1, -2)], c = st[o2(j1, 2)], d = st[o2(j1, 4)];
+            fma2(w2[0], a, ua);
+            fma2(w2[1], b, ua);
+            fma2(w2[2], c, ua);
+            fma2(w2[3], d, ua);
+          }
           asm volatile("" ::: "memory");
-          const double2 a3m4 = st[o3(-4)], a3m2 = st[o3(-2)], a3p2 = st[o3(2)], a3p4 = st[o3(4)];
-          fma2(w3[0], a3m4, u);
-          fma2(w3[1], a3m2, u);
-          fma2(w3[2], a3p2, u);
-          fma2(w3[3], a3p4, u);
+          {
+            const double2 a = st[oc - 4], b = st[oc - 2], c = st[oc + 2], d = st[oc + 4];
+            fma2(w3[0], a, ua);
+            fma2(w3[1], b, ua);
+            fma2(w3[2], c, ua);
+            fma2(w3[3], d, ua);
+          }
+          if (NP == 2) {
+            asm volatile("" ::: "memory");
+            {
+              const double2 a = st[o2(j1 + 2, -4)], b = st[o2(j1 + 2, -2)], c = st[o2(j1 + 2, 2)],
+                            d = st[o2(j1 + 2, 4)];
+              fma2(w2[0], a, ub);
+              fma2(w2[1], b, ub);
+              fma2(w2[2], c, ub);
+              fma2(w2[3], d, ub);
+            }
+            asm volatile("" ::: "memory");
+            {
+              const int ob = oc + 2 * R1;
+              const double2 a = st[ob - 4], b = st[ob - 2], c = st[ob + 2], d = st[ob + 4];
+              fma2(w3[0], a, ub);
+              fma2(w3[1], b, ub);
+              fma2(w3[2], c, ub);
+              fma2(w3[3], d, ub);
+            }
+          }
           __syncwarp();
           if (lane == 0) f1_mbar_arrive(&empty[cs]);
           if (++cs == F1_S) {
@@ -272,28 +339,37 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
           const double2 wb = *(const double2*)(W + p * F1_WROW + 2);
           const double2 wc = *(const double2*)(W + p * F1_WROW + 4);
           const double2 wd = *(const double2*)(W + p * F1_WROW + 6);
-          fma2(wa.x, c, u);
-          R[U].x += u.x;
-          R[U].y += u.y;
-          fma2(wa.y, c, R[(U + 2) % 9]);
-          fma2(wb.x, c, R[(U + 7) % 9]);
-          fma2(wb.y, c, R[(U + 4) % 9]);
-          fma2(wc.x, c, R[(U + 5) % 9]);
-          if (NMIX) {
-            double2 g = make_double2(wg0 * gm.x, wg0 * gm.y);
-            fma2(wg1, gp, g);
-            fma2(wc.y, g, R[(U + 1) % 9]);
-            fma2(wd.x, g, R[(U + 8) % 9]);
-          }
+          auto scatter = [&](double2* R, double2 c, double2 u, double2 g) {
+            fma2(wa.x, c, u);
+            R[U].x += u.x;
+            R[U].y += u.y;
+            fma2(wa.y, c, R[(U + 2) % 9]);
+            fma2(wb.x, c, R[(U + 7) % 9]);
+            fma2(wb.y, c, R[(U + 4) % 9]);
+            fma2(wc.x, c, R[(U + 5) % 9]);
+            if (NMIX) {
+              fma2(wc.y, g, R[(U + 1) % 9]);
+              fma2(wd.x, g, R[(U + 8) % 9]);
+            }
+          };
+          scatter(RA, ca, ua, ga);
+          if (NP == 2) scatter(RB, cb, ub, gb);
         }
         // y(p - 4) has received its last contribution
         constexpr int SQ = (U + 5) % 9;
-        if (p >= F1_H && inside) {
-          const int64_t gi = (int64_t)(p - F1_H) * plane + col;
-          y[gi] = R[SQ];
-          if (DOT) cdot_acc(__ldg(v + gi), R[SQ], dacc);
+        if (p >= F1_H) {
+          const int64_t base = (int64_t)(p - F1_H) * plane;
+          if (in0) {
+            y[base + col] = RA[SQ];
+            if (DOT) cdot_acc(__ldg(v + base + col), RA[SQ], dacc);
+          }
+          if (NP == 2 && in1) {
+            y[base + colb] = RB[SQ % (NP == 2 ? 9 : 1)];
+            if (DOT) cdot_acc(__ldg(v + base + colb), RB[SQ % (NP == 2 ? 9 : 1)], dacc);
+          }
         }
-        R[SQ] = make_double2(0.0, 0.0);
+        RA[SQ] = make_double2(0.0, 0.0);
+        if (NP == 2) RB[SQ % (NP == 2 ? 9 : 1)] = make_double2(0.0, 0.0);
       });
     }
   }

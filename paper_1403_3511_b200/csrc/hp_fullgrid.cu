@@ -266,6 +266,22 @@ static bool fg_single_enabled() {
   return v == 1;
 }
 
+static int fg_np() {  // points per thread of the single-pass kernel (HP_FG_NP = 1 or 2)
+  static int v = [] {
+    const char* e = getenv("HP_FG_NP");
+    return e && atoi(e) == 1 ? 1 : 2;
+  }();
+  return v;
+}
+static int fg_exp() {  // timing experiments only (HP_FG_EXP bit 0: skip halo boxes, bit 1: skip
+                       // compute -> wrong results)
+  static int v = [] {
+    const char* e = getenv("HP_FG_EXP");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 static int sm_count() {
   static int n = [] {
     int dev = 0, c = 148;
@@ -279,9 +295,8 @@ template <int NMIX>
 static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, const double* P, const double* G,
                                const FgPlan& F, cudaStream_t st, DotOut* dot, bool* launched) {
   *launched = false;
-  CUtensorMap mA1, mA3, mB2;
-  if (!tma_map(&mA1, v, s->side, 2 * F1_T, F1_T, F1_T + 2 * F1_H) ||
-      !tma_map(&mA3, v, s->side, 2 * F1_H, F1_T, F1_T) || !tma_map(&mB2, v, s->side, 2 * F1_T, F1_H, F1_T))
+  CUtensorMap mA1, mB2;
+  if (!tma_map(&mA1, v, s->side, 2 * F1_RW, F1_T, F1_T + 2 * F1_H) || !tma_map(&mB2, v, s->side, 2 * F1_T, F1_H, F1_T))
     return HP_OK;  // no driver entry point: the two-pass kernels run
   hp_status rc = ensure_tiles(s);
   if (rc) return rc;
@@ -289,10 +304,12 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
   const double* B0 = s->fg_basis + (size_t)(NMIX ? F.r0[0] : 0) * n0 * FG_W;  // axis 0, degree r0
   const int grid = std::min(s->fg_ntiles, sm_count());
   const bool use_dot = dot && dot->partial && grid <= dot->capacity;
-  auto kern = use_dot ? k_fg_single<NMIX, true> : k_fg_single<NMIX, false>;
+  const int np = fg_np();
+  auto kern = np == 1 ? (use_dot ? k_fg_single<NMIX, true, 1> : k_fg_single<NMIX, false, 1>)
+                      : (use_dot ? k_fg_single<NMIX, true, 2> : k_fg_single<NMIX, false, 2>);
   HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F1_SMEM));
-  kern<<<grid, F1_THREADS, F1_SMEM, st>>>(mA1, mA3, mB2, v, y, P, G, B0, s->fg_tiles, s->fg_ntiles, n0,
-                                          s->side[1], s->side[2], s->side[3], use_dot ? dot->partial : nullptr);
+  kern<<<grid, F1_POINTS / np, F1_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles, s->fg_ntiles, n0, s->side[1],
+                                              s->side[2], s->side[3], use_dot ? dot->partial : nullptr, fg_exp());
   HP_LAUNCH_CHECK("k_fg_single");
   if (use_dot) dot->n = grid;
   *launched = true;
