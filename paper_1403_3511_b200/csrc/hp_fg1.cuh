@@ -29,17 +29,24 @@
 
 #include <cuda.h>
 
+#ifndef F1_TILE_J2
+#define F1_TILE_J2 4
+#endif
+
 namespace hp {
 
-constexpr int F1_T = 8;                 // tile edge along axes 1, 2, 3
+// tile extents along axes 1, 2, 3 (T1 must be 8: the NP = 2 row pairing assumes it)
+constexpr int F1_T1 = 8;
+constexpr int F1_T2 = F1_TILE_J2;
+constexpr int F1_T3 = 64 / F1_TILE_J2;
 constexpr int F1_H = FG_K;              // halo (band radius)
 constexpr int F1_S = 5;                 // pipeline stages
-constexpr int F1_POINTS = F1_T * F1_T * F1_T;  // tile points (512)
+constexpr int F1_POINTS = F1_T1 * F1_T2 * F1_T3;  // tile points (512)
 // stage layout in double2 units: A1 = [j1 +-4][j2][j3 +-4] (256 B rows: the j3 halos ride in the
 // tile rows -- 64 B halo rows cost the TMA unit twice as much per byte) | j2 halos lo, hi
-constexpr int F1_RW = F1_T + 2 * F1_H;                   // A1 row (j3) length
-constexpr int F1_A1 = (F1_T + 2 * F1_H) * F1_T * F1_RW;  // 2048
-constexpr int F1_B2 = F1_T * F1_H * F1_T;                // 256  ([j1][4][j3])
+constexpr int F1_RW = F1_T3 + 2 * F1_H;                    // A1 row (j3) length
+constexpr int F1_A1 = (F1_T1 + 2 * F1_H) * F1_T2 * F1_RW;  // [j1 +-4][j2][j3 +-4]
+constexpr int F1_B2 = F1_T1 * F1_H * F1_T3;                // [j1][4][j3]
 constexpr int F1_OFF_B2LO = F1_A1;
 constexpr int F1_OFF_B2HI = F1_A1 + F1_B2;
 constexpr int F1_STAGE = F1_A1 + 2 * F1_B2;  // 2560 double2 = 40 KB
@@ -130,7 +137,7 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
   uint64_t* full = (uint64_t*)(f1_smem + F1_BOFF);
   uint64_t* empty = full + F1_S;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int j3 = tid & 7, j2 = (tid >> 3) & 7;
+  const int j3 = tid % F1_T3, j2 = (tid / F1_T3) % F1_T2;
   const int j1 = NP == 1 ? (tid >> 6) : (((tid >> 6) >> 1) * 4 + ((tid >> 6) & 1));  // first row
   const double* P0 = P;
   const double* P1 = P + FG_MAXN * FG_W;
@@ -173,9 +180,9 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
     if (pu > 0) f1_mbar_wait(&empty[ps], (unsigned)((pu - 1) & 1));
     if (pp == 0) {
       const int code = __ldg(tiles + blockIdx.x + pti * gridDim.x);
-      ps_[5] = (code & 1023) * F1_T;
-      ps_[6] = ((code >> 10) & 1023) * F1_T;
-      ps_[7] = (code >> 20) * F1_T;
+      ps_[5] = (code & 1023) * F1_T1;
+      ps_[6] = ((code >> 10) & 1023) * F1_T2;
+      ps_[7] = (code >> 20) * F1_T3;
     }
     const int T1 = ps_[5], T2 = ps_[6], T3 = ps_[7];
     double2* dst = stg + (size_t)ps * F1_STAGE;
@@ -189,12 +196,12 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
       const uint64_t pol = f1_policy(hint);
       f1_tma4_hint(dst, &mA1, 2 * (T3 - F1_H), T2, T1 - F1_H, pp, bar, pol);
       f1_tma4_hint(dst + F1_OFF_B2LO, &mB2, 2 * T3, T2 - F1_H, T1, pp, bar, pol);
-      f1_tma4_hint(dst + F1_OFF_B2HI, &mB2, 2 * T3, T2 + F1_T, T1, pp, bar, pol);
+      f1_tma4_hint(dst + F1_OFF_B2HI, &mB2, 2 * T3, T2 + F1_T2, T1, pp, bar, pol);
     } else {
       f1_tma4(dst, &mA1, 2 * (T3 - F1_H), T2, T1 - F1_H, pp, bar);
       if (!(exp & 1)) {
         f1_tma4(dst + F1_OFF_B2LO, &mB2, 2 * T3, T2 - F1_H, T1, pp, bar);
-        f1_tma4(dst + F1_OFF_B2HI, &mB2, 2 * T3, T2 + F1_T, T1, pp, bar);
+        f1_tma4(dst + F1_OFF_B2HI, &mB2, 2 * T3, T2 + F1_T2, T1, pp, bar);
       }
     }
     ++pk;
@@ -215,15 +222,15 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
   if (tid == 0)
     for (int k = 0; k < F1_S - 1; ++k) issue_next();
 
-  constexpr int R1 = F1_T * F1_RW;  // A1 j1-row stride (double2)
+  constexpr int R1 = F1_T2 * F1_RW;  // A1 j1-row stride (double2)
   // centre of point 0 in A1; point 1 (NP = 2) sits two j1 rows below
   const int oc = (j1 + F1_H) * R1 + j2 * F1_RW + j3 + F1_H;
   // axis-2 taps: inside the tile they are A1 rows, outside they live in the j2 halo boxes
   // (computed on the fly so they hold no registers across the march)
   auto o2 = [&](int row, int d) {
     const int a = j2 + d;
-    return a < 0 ? F1_OFF_B2LO + row * 32 + (a + F1_H) * 8 + j3
-                 : (a >= F1_T ? F1_OFF_B2HI + row * 32 + (a - F1_T) * 8 + j3
+    return a < 0 ? F1_OFF_B2LO + row * (F1_H * F1_T3) + (a + F1_H) * F1_T3 + j3
+                 : (a >= F1_T2 ? F1_OFF_B2HI + row * (F1_H * F1_T3) + (a - F1_T2) * F1_T3 + j3
                               : (row + F1_H) * R1 + a * F1_RW + j3 + F1_H);
   };
 
@@ -232,8 +239,8 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
   const int64_t plane = (int64_t)n1 * n2 * n3;
   for (int ti = 0; ti < my_tiles; ++ti) {
     const int code = __ldg(tiles + blockIdx.x + ti * gridDim.x);
-    const int J1 = (code & 1023) * F1_T + j1, J2 = ((code >> 10) & 1023) * F1_T + j2,
-              J3 = (code >> 20) * F1_T + j3;
+    const int J1 = (code & 1023) * F1_T1 + j1, J2 = ((code >> 10) & 1023) * F1_T2 + j2,
+              J3 = (code >> 20) * F1_T3 + j3;
     const bool in0 = J1 < n1 && J2 < n2 && J3 < n3;
     const bool in1 = NP == 2 && J1 + 2 < n1 && J2 < n2 && J3 < n3;
     const int c1a = min(J1, FG_MAXN - 1), c1b = min(J1 + 2, FG_MAXN - 1);

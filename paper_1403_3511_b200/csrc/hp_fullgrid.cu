@@ -240,8 +240,8 @@ static bool tma_map(CUtensorMap* m, const void* base, const int side[4], unsigne
 static hp_status ensure_tiles(const hp_set_s* s) {
   std::lock_guard<std::mutex> g(s->fg_mtx);
   if (s->fg_tiles) return HP_OK;
-  const int t1 = (s->side[1] + F1_T - 1) / F1_T, t2 = (s->side[2] + F1_T - 1) / F1_T,
-            t3 = (s->side[3] + F1_T - 1) / F1_T;
+  const int t1 = (s->side[1] + F1_T1 - 1) / F1_T1, t2 = (s->side[2] + F1_T2 - 1) / F1_T2,
+            t3 = (s->side[3] + F1_T3 - 1) / F1_T3;
   constexpr int BE = 3;
   std::vector<int> codes;
   codes.reserve((size_t)t1 * t2 * t3);
@@ -296,7 +296,8 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
                                const FgPlan& F, cudaStream_t st, DotOut* dot, bool* launched) {
   *launched = false;
   CUtensorMap mA1, mB2;
-  if (!tma_map(&mA1, v, s->side, 2 * F1_RW, F1_T, F1_T + 2 * F1_H) || !tma_map(&mB2, v, s->side, 2 * F1_T, F1_H, F1_T))
+  if (!tma_map(&mA1, v, s->side, 2 * F1_RW, F1_T2, F1_T1 + 2 * F1_H) ||
+      !tma_map(&mB2, v, s->side, 2 * F1_T3, F1_H, F1_T1))
     return HP_OK;  // no driver entry point: the two-pass kernels run
   hp_status rc = ensure_tiles(s);
   if (rc) return rc;
