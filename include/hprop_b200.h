@@ -126,6 +126,18 @@ hp_status hp_apply_polynomial(hp_set_t s, const int32_t* degrees_host, const dou
                               const int32_t* axis_order_host, void* workspace_dev,
                               size_t workspace_bytes, void* stream);
 
+/* apply_polynomial on HOST-resident vectors (the reference's numpy arrays live in host memory:
+ * fast_apply.py:110-164 takes and returns ndarrays).  in_host/out_host: n*batch elements, pinned
+ * for overlap; in_dev/out_dev: device buffers of the same size.  On full cubes of the fused
+ * class the copies run in j1-plane chunks on internal streams, overlapped with the kernels
+ * (input chunk k+1 in flight while chunk k is computed and chunk k-1 copied out); otherwise
+ * whole-vector copies around hp_apply_polynomial.  Ordered on `stream`; returns once queued. */
+hp_status hp_apply_polynomial_streamed(hp_set_t s, const int32_t* degrees_host, const double* coeffs_host,
+                                       int nterms, double halfwidth, int dtype, const void* in_host,
+                                       void* out_host, void* in_dev, void* out_dev, int64_t batch,
+                                       int flags, void* workspace_dev, size_t workspace_bytes,
+                                       void* stream);
+
 /* apply_square_sum -- fast_apply.py:202-245 (exact restricted sum_l x_l^2) */
 hp_status hp_square_sum(hp_set_t s, int dtype, const void* in_dev, void* out_dev,
                         int64_t batch, void* stream);

@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
     k_fg_single(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB2,
                 const double2* __restrict__ v, double2* __restrict__ y, const double* __restrict__ P,
                 const double* __restrict__ G, const double* __restrict__ B0, const int* __restrict__ tiles,
-                int ntiles, int n0, int n1, int n2, int n3, double2* __restrict__ dotp, int exp) {
+                int ntiles, int n0, int n1, int n2, int n3, double2* __restrict__ dotp, int exp, int plo,
+                int phi) {
   constexpr int NT = F1_POINTS / NP;
   extern __shared__ __align__(128) unsigned char f1_smem[];
   double2* stg = (double2*)f1_smem;
@@ -168,17 +169,22 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
   __syncthreads();
 
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int nitems = my_tiles * n0;
+  // output planes [plo, phi) (the whole cube, or one chunk of a streamed matvec): the march
+  // consumes input planes [ps0, pe), the band radius around them
+  const int ps0 = max(plo - F1_H, 0), pe = min(phi + F1_H, n0), nper = pe - ps0;
+  const int nitems = my_tiles * nper;
   // producer state (thread 0 only; kept in shared memory so that it costs the consumer
   // threads no registers): next item, its tile / plane / stage / stage-use count, tile origin
   int* ps_ = (int*)(empty + F1_S);
-  if (tid == 0)
+  if (tid == 0) {
     for (int i = 0; i < 8; ++i) ps_[i] = 0;
+    ps_[2] = ps0;
+  }
   auto issue_next = [&]() {
     int pk = ps_[0], pti = ps_[1], pp = ps_[2], ps = ps_[3], pu = ps_[4];
     if (pk >= nitems) return;
     if (pu > 0) f1_mbar_wait(&empty[ps], (unsigned)((pu - 1) & 1));
-    if (pp == 0) {
+    if (pp == ps0) {
       const int code = __ldg(tiles + blockIdx.x + pti * gridDim.x);
       ps_[5] = (code & 1023) * F1_T1;
       ps_[6] = ((code >> 10) & 1023) * F1_T2;
@@ -205,8 +211,8 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
       }
     }
     ++pk;
-    if (++pp == n0) {
-      pp = 0;
+    if (++pp == pe) {
+      pp = ps0;
       ++pti;
     }
     if (++ps == F1_S) {
@@ -277,21 +283,21 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
 #pragma unroll
     for (int i = 0; i < (NP == 2 ? 9 : 1); ++i) RB[i] = make_double2(0.0, 0.0);
 
-    for (int pb = 0; pb < n0 + F1_H; pb += 9) {
+    for (int pb = ps0 - ps0 % 9; pb < phi + F1_H; pb += 9) {  // ring slot = plane mod 9
       unroll<9>([&](auto UU) {
         constexpr int U = decltype(UU)::value;
         const int p = pb + U;
-        if (p >= n0 + F1_H) return;
+        if (p < ps0 || p >= phi + F1_H) return;
         // DOT: v at the plane completed by this step is re-read from L2 (it was staged 4 planes
         // ago); the load is issued here, ahead of the stage wait and the step's work, so its
         // latency is hidden (the wait's memory clobber keeps the compiler from sinking it)
         double2 vqa = make_double2(0.0, 0.0), vqb = make_double2(0.0, 0.0);
-        if (DOT && p >= F1_H) {
+        if (DOT && p - F1_H >= plo) {
           const int64_t base = (int64_t)(p - F1_H) * plane;
           if (in0) vqa = __ldg(v + base + col);
           if (NP == 2 && in1) vqb = __ldg(v + base + colb);
         }
-        if (p < n0) {
+        if (p < pe) {
           if (tid == 0) issue_next();
           f1_mbar_wait(&full[cs], (unsigned)(cu & 1));
           if (exp & 2) {  // timing experiment: pipeline only
@@ -402,7 +408,7 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
         }
         // y(p - 4) has received its last contribution
         constexpr int SQ = (U + 5) % 9;
-        if (p >= F1_H) {
+        if (p - F1_H >= plo) {
           const int64_t base = (int64_t)(p - F1_H) * plane;
           if (in0) {
             __stcs(y + base + col, RA[SQ]);  // streaming store: keep L2 for v halos

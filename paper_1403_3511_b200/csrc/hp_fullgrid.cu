@@ -293,7 +293,9 @@ static int sm_count() {
 
 template <int NMIX>
 static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, const double* P, const double* G,
-                               const FgPlan& F, cudaStream_t st, DotOut* dot, bool* launched) {
+                               const FgPlan& F, cudaStream_t st, DotOut* dot, bool* launched, int plo = 0,
+                               int phi = -1) {
+  if (phi < 0) phi = s->side[0];
   *launched = false;
   CUtensorMap mA1, mB2;
   if (!tma_map(&mA1, v, s->side, 2 * F1_RW, F1_T2, F1_T1 + 2 * F1_H) ||
@@ -310,7 +312,8 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
                       : (use_dot ? k_fg_single<NMIX, true, 2> : k_fg_single<NMIX, false, 2>);
   HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F1_SMEM));
   kern<<<grid, F1_POINTS / np, F1_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles, s->fg_ntiles, n0, s->side[1],
-                                              s->side[2], s->side[3], use_dot ? dot->partial : nullptr, fg_exp());
+                                              s->side[2], s->side[3], use_dot ? dot->partial : nullptr, fg_exp(),
+                                              plo, phi);
   HP_LAUNCH_CHECK("k_fg_single");
   if (use_dot) dot->n = grid;
   *launched = true;
@@ -377,12 +380,13 @@ size_t fullgrid_workspace_bytes(const hp_set_s* s, const std::vector<Term>& term
   return (size_t)(4 + 2) * FG_MAXN * FG_W * sizeof(double) + 256 + (size_t)s->n * sizeof(double2);
 }
 
-hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
-                         const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
-                         cudaStream_t st, bool* done, DotOut* dot) {
-  if (dot) dot->n = 0;
-  *done = false;
-  FgPlan F = classify(s, terms, dtype, batch, flags);
+// classification + band tables; *ok = false when the fused evaluator does not cover the call
+static hp_status fg_prepare(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
+                            int64_t batch, int flags, void* ws, size_t ws_bytes, cudaStream_t st, FgPlan* Fo,
+                            bool* ok) {
+  *ok = false;
+  FgPlan& F = *Fo;
+  F = classify(s, terms, dtype, batch, flags);
   if (!F.ok) return HP_OK;
   size_t need = fullgrid_workspace_bytes(s, terms, dtype, batch, flags);
   if (ws_bytes < need) return HP_OK;  // caller sized for the generic program only
@@ -390,7 +394,6 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   if (rc) return rc;
   double* P = (double*)ws;
   double* G = P + 4 * FG_MAXN * FG_W;
-  double2* u = (double2*)((char*)ws + (((size_t)6 * FG_MAXN * FG_W * sizeof(double) + 255) & ~(size_t)255));
   CombineArgs A;
   for (int a = 0; a < 4; ++a) {
     for (int k = 0; k <= FG_K; ++k) A.ws[a][k] = F.ws[a][k];
@@ -404,12 +407,35 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   A.osc = (flags & HP_ADD_OSC) ? 1 : 0;
   k_fg_combine<<<64, 256, 0, st>>>(s->fg_basis, P, G, A);
   HP_LAUNCH_CHECK("k_fg_combine");
+  *ok = true;
+  return HP_OK;
+}
+
+// the single-pass kernel covers even single-axis bands and at most one r1 = 1 coupling class
+static bool fg_single_class(const FgPlan& F) {
+  const bool even = F.mask[0] == FG_MASK_EVEN && F.mask[1] == FG_MASK_EVEN && F.mask[2] == FG_MASK_EVEN &&
+                    F.mask[3] == FG_MASK_EVEN;
+  return fg_single_enabled() && even &&
+         (F.nmix == 0 || (F.nmix == 1 && F.rm == 1 && (F.maskG & ~FG_MASK_PM1) == 0));
+}
+
+hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
+                         const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
+                         cudaStream_t st, bool* done, DotOut* dot) {
+  if (dot) dot->n = 0;
+  *done = false;
+  FgPlan F;
+  bool ok = false;
+  hp_status rc = fg_prepare(s, terms, halfwidth, dtype, batch, flags, ws, ws_bytes, st, &F, &ok);
+  if (rc || !ok) return rc;
+  double* P = (double*)ws;
+  double* G = P + 4 * FG_MAXN * FG_W;
+  double2* u = (double2*)((char*)ws + (((size_t)6 * FG_MAXN * FG_W * sizeof(double) + 255) & ~(size_t)255));
   const double2* v = (const double2*)in;
   double2* y = (double2*)out;
   const bool even = F.mask[0] == FG_MASK_EVEN && F.mask[2] == FG_MASK_EVEN && F.mask[3] == FG_MASK_EVEN;
   // single pass for the even-band class (cfg4)
-  if (fg_single_enabled() && even && F.mask[1] == FG_MASK_EVEN &&
-      (F.nmix == 0 || (F.nmix == 1 && F.rm == 1 && (F.maskG & ~FG_MASK_PM1) == 0))) {
+  if (fg_single_class(F)) {
     bool launched = false;
     rc = F.nmix ? launch_single<1>(s, v, y, P, G, F, st, dot, &launched)
                 : launch_single<0>(s, v, y, P, G, F, st, dot, &launched);
@@ -438,6 +464,86 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   else
     rc = launch_outer<2, 2, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st, dot);
   if (rc) return rc;
+  *done = true;
+  return HP_OK;
+}
+
+
+// ---------------------------------------------------------------- streamed (host-resident vectors)
+
+// copy streams of the streamed matvec, one pair per device
+static hp_status copy_streams(cudaStream_t* in, cudaStream_t* out) {
+  static std::mutex mtx;
+  static std::map<int, std::pair<cudaStream_t, cudaStream_t>> per_dev;
+  int dev = 0;
+  HP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mtx);
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    cudaStream_t a, b;
+    HP_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+    HP_CUDA(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+    it = per_dev.emplace(dev, std::make_pair(a, b)).first;
+  }
+  *in = it->second.first;
+  *out = it->second.second;
+  return HP_OK;
+}
+
+// y = W v for host-resident v / y on a full cube of the single-pass class.  The cube is cut
+// into chunks of j1 planes (>= 4, ~128 MB); chunk k is copied in on one stream, its output
+// planes are computed on `st` once chunk k+1 (the band halo) has landed, and copied out on a
+// third stream, so PCIe traffic in both directions overlaps the kernels.  *done = false when
+// the set / terms are not covered (the caller then copies whole vectors).
+hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
+                                  const void* in_host, void* out_host, void* in_dev, void* out_dev, int flags,
+                                  void* ws, size_t ws_bytes, cudaStream_t st, bool* done) {
+  *done = false;
+  FgPlan F = classify(s, terms, dtype, 1, flags);
+  if (!F.ok || !fg_single_class(F)) return HP_OK;
+  bool ok = false;
+  hp_status rc = fg_prepare(s, terms, halfwidth, dtype, 1, flags, ws, ws_bytes, st, &F, &ok);
+  if (rc || !ok) return rc;
+  const double* P = (const double*)ws;
+  const double* G = P + 4 * FG_MAXN * FG_W;
+  const int n0 = s->side[0];
+  const size_t plane = (size_t)(s->n / n0) * sizeof(double2);
+  int C = (int)std::min<size_t>(n0, ((size_t)128 << 20) / std::max<size_t>(plane, 1));
+  if (const char* e = getenv("HP_STREAM_CHUNK")) C = atoi(e);  // planes per chunk (tests)
+  C = std::max(C, F1_H);  // chunk k+1 must cover the band halo of chunk k
+  const int nch = (n0 + C - 1) / C;
+  cudaStream_t sin, sout;
+  if ((rc = copy_streams(&sin, &sout))) return rc;
+  std::vector<cudaEvent_t> ev(2 * nch + 2);
+  for (auto& e : ev) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t ev0 = ev[2 * nch], evend = ev[2 * nch + 1];
+  HP_CUDA(cudaEventRecord(ev0, st));  // orders the copies after the caller's prior work
+  HP_CUDA(cudaStreamWaitEvent(sin, ev0, 0));
+  HP_CUDA(cudaStreamWaitEvent(sout, ev0, 0));
+  for (int k = 0; k < nch; ++k) {
+    const int p0 = k * C, p1 = std::min(n0, p0 + C);
+    HP_CUDA(cudaMemcpyAsync((char*)in_dev + p0 * plane, (const char*)in_host + p0 * plane, (p1 - p0) * plane,
+                            cudaMemcpyHostToDevice, sin));
+    HP_CUDA(cudaEventRecord(ev[k], sin));
+  }
+  for (int k = 0; k < nch; ++k) {
+    const int p0 = k * C, p1 = std::min(n0, p0 + C);
+    HP_CUDA(cudaStreamWaitEvent(st, ev[std::min(k + 1, nch - 1)], 0));
+    bool launched = false;
+    rc = F.nmix ? launch_single<1>(s, (const double2*)in_dev, (double2*)out_dev, P, G, F, st, nullptr, &launched,
+                                   p0, p1)
+                : launch_single<0>(s, (const double2*)in_dev, (double2*)out_dev, P, G, F, st, nullptr, &launched,
+                                   p0, p1);
+    if (rc) return rc;
+    if (!launched) return fail(HP_ERR_RUNTIME, "streamed matvec: TMA descriptors unavailable");
+    HP_CUDA(cudaEventRecord(ev[nch + k], st));
+    HP_CUDA(cudaStreamWaitEvent(sout, ev[nch + k], 0));
+    HP_CUDA(cudaMemcpyAsync((char*)out_host + p0 * plane, (const char*)out_dev + p0 * plane, (p1 - p0) * plane,
+                            cudaMemcpyDeviceToHost, sout));
+  }
+  HP_CUDA(cudaEventRecord(evend, sout));
+  HP_CUDA(cudaStreamWaitEvent(st, evend, 0));
+  for (auto& e : ev) cudaEventDestroy(e);  // released once the recorded work completes
   *done = true;
   return HP_OK;
 }

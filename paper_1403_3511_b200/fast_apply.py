@@ -181,6 +181,43 @@ class PolynomialApplier:
             float(approx.halfwidth), dtype, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), batch,
             flags, None, ctypes.c_void_p(ws.data_ptr()), ws.numel(), nat.stream_ptr()))
 
+    def apply_host_into(self, approx, x_host, y_host, flags: int = 0) -> None:
+        """Host-resident vectors: y_host <- W(X) x_host for CPU tensors (pin them for overlap).
+
+        One C-ABI call (hp_apply_polynomial_streamed): on full cubes of the fused class the
+        library streams j1-plane chunks in, computes each chunk once its halo has landed and
+        streams the result out, so both PCIe directions overlap the kernels.  Device buffers
+        and the workspace are cached per (approx, shape, flags).  Ordered on the current
+        stream; synchronise before reading y_host.
+        """
+        import torch
+
+        if x_host.is_cuda or y_host.is_cuda or x_host.shape != y_host.shape or x_host.dtype != y_host.dtype:
+            raise ValueError("apply_host_into expects two CPU tensors of the same shape and dtype")
+        if not (x_host.is_contiguous() and y_host.is_contiguous()):
+            raise ValueError("apply_host_into expects contiguous tensors")
+        key = ("host", id(approx), tuple(x_host.shape), x_host.dtype, flags)
+        cache = self.__dict__.setdefault("_into_cache", {})
+        ent = cache.get(key)
+        if ent is None:
+            degs, coeffs = _term_arrays(approx, self.iset.dim)
+            batch = 1 if x_host.dim() == 1 else x_host.shape[0]
+            dtype = nat.HP_C128 if x_host.is_complex() else nat.HP_F64
+            h = ctypes.c_void_p(self.iset.handle)
+            wsb = nat.lib().hp_poly_workspace_bytes(h, degs.ctypes.data_as(nat.c_i32p), degs.shape[0], dtype,
+                                                    batch, flags)
+            ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device="cuda")
+            xd = torch.empty(x_host.shape, dtype=x_host.dtype, device="cuda")
+            yd = torch.empty_like(xd)
+            ent = (approx, degs, coeffs, h, batch, dtype, ws, xd, yd)
+            cache[key] = ent
+        _, degs, coeffs, h, batch, dtype, ws, xd, yd = ent
+        nat.check(nat.lib().hp_apply_polynomial_streamed(
+            h, degs.ctypes.data_as(nat.c_i32p), coeffs.ctypes.data_as(nat.c_dblp), degs.shape[0],
+            float(approx.halfwidth), dtype, ctypes.c_void_p(x_host.data_ptr()), ctypes.c_void_p(y_host.data_ptr()),
+            ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(yd.data_ptr()), batch, flags,
+            ctypes.c_void_p(ws.data_ptr()), ws.numel(), nat.stream_ptr()))
+
     def apply_polynomial(self, approx: ChebApprox, v, axis_order=None, *, ref_order: bool = False):
         """Multiply v by the restricted Galerkin matrix of the surrogate."""
         flags = nat.HP_REF_ORDER if ref_order else 0

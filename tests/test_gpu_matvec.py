@@ -398,3 +398,45 @@ def test_random_term_structures_vs_oracle(hp, seed):
     Y = appl.apply_polynomial(ap, V)
     for b in range(3):
         assert rel_l2(Y[b], oa.polynomial(degs, coeffs, 16.0, V[b])) < TOL
+
+
+@pytest.mark.parametrize("bound,chunk", [(11, 4), (11, 5), (20, 7), (20, 64)])
+def test_streamed_host_matvec_matches_device(hp, bound, chunk, monkeypatch):
+    """hp_apply_polynomial_streamed (host-resident vectors, j1-plane chunks overlapped with the
+    kernels) gives bit-for-bit the device matvec, for chunkings that do and do not divide n0."""
+    import torch
+
+    monkeypatch.setenv("HP_STREAM_CHUNK", str(chunk))
+    w = W.CONFIGS["cfg4"].scaled(bound, "cfg4x")
+    ap = w.approx(0.3)
+    c = W.coefficients(w)
+    s = hp.build_full(w.dim, w.bound)
+    appl = hp.get_applier(s)
+    for flags in (0, 1):  # polynomial, Hamiltonian
+        xd = torch.from_numpy(c).cuda()
+        yd = torch.empty_like(xd)
+        appl.apply_into(ap, xd, yd, flags)
+        xh = torch.from_numpy(c).pin_memory()
+        yh = torch.zeros_like(xh).pin_memory()
+        appl.apply_host_into(ap, xh, yh, flags)
+        torch.cuda.synchronize()
+        assert torch.equal(yh, yd.cpu())
+    oa = O.applier_for_full(w.dim, w.bound)
+    assert rel_l2(yh.numpy(), oa.hamiltonian(ap.degrees, ap.coeffs, 16.0, c)) < TOL
+
+
+def test_streamed_host_matvec_fallback_sets(hp):
+    """Sets outside the fused class (hyperbolic, real vectors) take whole-vector copies."""
+    import torch
+
+    s = hp.build_hyperbolic(3, 12)
+    ap = _approx(np.array([[0, 0, 0], [2, 0, 0], [1, 1, 0], [0, 0, 4]]), np.array([1.0, 0.5, -0.25, 0.1]), 3, degree=4)
+    appl = hp.get_applier(s)
+    gen = np.random.default_rng(7)
+    for cplx in (True, False):
+        v = gen.standard_normal(s.size) + (1j * gen.standard_normal(s.size) if cplx else 0.0)
+        xh = torch.from_numpy(v).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        appl.apply_host_into(ap, xh, yh)
+        torch.cuda.synchronize()
+        assert np.array_equal(yh.numpy(), appl.apply_polynomial(ap, v))
