@@ -29,6 +29,18 @@
 
 #include <cuda.h>
 
+// compiler fence between the stage's load groups (bounds registers held by in-flight loads)
+#ifndef F1_FENCES
+#define F1_FENCES 0
+#endif
+#if F1_FENCES
+#define F1_FENCE() asm volatile("" ::: "memory")
+#else
+#define F1_FENCE() \
+  do {             \
+  } while (0)
+#endif
+
 #ifndef F1_TILE_J2
 #define F1_TILE_J2 4
 #endif
@@ -182,7 +194,7 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
   }
   auto issue_next = [&]() {
     int pk = ps_[0], pti = ps_[1], pp = ps_[2], ps = ps_[3], pu = ps_[4];
-    if (pk >= nitems) return;
+    if (pk >= nitems || (exp & 8)) return;
     if (pu > 0) f1_mbar_wait(&empty[ps], (unsigned)((pu - 1) & 1));
     if (pp == ps0) {
       const int code = __ldg(tiles + blockIdx.x + pti * gridDim.x);
@@ -299,7 +311,7 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
         }
         if (p < pe) {
           if (tid == 0) issue_next();
-          f1_mbar_wait(&full[cs], (unsigned)(cu & 1));
+          if (!(exp & 8)) f1_mbar_wait(&full[cs], (unsigned)(cu & 1));  // bit 3: compute only
           if (exp & 2) {  // timing experiment: pipeline only
             __syncwarp();
             if (lane == 0) f1_mbar_arrive(&empty[cs]);
@@ -334,7 +346,7 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
             }
           }
           if (NMIX) {
-            asm volatile("" ::: "memory");
+            F1_FENCE();
             const double2 m1 = st[oc - R1], p1 = st[oc + R1];
             ga = make_double2(wga0 * m1.x, wga0 * m1.y);
             fma2(wga1, p1, ga);
@@ -344,7 +356,7 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
               fma2(wgb1, p3, gb);
             }
           }
-          asm volatile("" ::: "memory");
+          F1_FENCE();
           {
             const double2 a = st[o2(j1, -4)], b = st[o2(j1, -2)], c = st[o2(j1, 2)], d = st[o2(j1, 4)];
             fma2(w2[0], a, ua);
@@ -352,7 +364,7 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
             fma2(w2[2], c, ua);
             fma2(w2[3], d, ua);
           }
-          asm volatile("" ::: "memory");
+          F1_FENCE();
           {
             const double2 a = st[oc - 4], b = st[oc - 2], c = st[oc + 2], d = st[oc + 4];
             fma2(w3[0], a, ua);
@@ -361,7 +373,7 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
             fma2(w3[3], d, ua);
           }
           if (NP == 2) {
-            asm volatile("" ::: "memory");
+            F1_FENCE();
             {
               const double2 a = st[o2(j1 + 2, -4)], b = st[o2(j1 + 2, -2)], c = st[o2(j1 + 2, 2)],
                             d = st[o2(j1 + 2, 4)];
@@ -370,7 +382,7 @@ __global__ void __launch_bounds__(F1_POINTS / NP, 1)
               fma2(w2[2], c, ub);
               fma2(w2[3], d, ub);
             }
-            asm volatile("" ::: "memory");
+            F1_FENCE();
             {
               const int ob = oc + 2 * R1;
               const double2 a = st[ob - 4], b = st[ob - 2], c = st[ob + 2], d = st[ob + 4];
