@@ -21,6 +21,7 @@
 // every term is unchanged, so on pruned sets the operator is the
 // reference's; only the summation order of the terms differs.
 #include <algorithm>
+#include <cstdio>
 #include <map>
 #include <vector>
 
@@ -270,6 +271,14 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut)
   return P;
 }
 
+static void dump_plan(const LvProgram& P) {  // HP_LEVEL_DEBUG=1: planner output on stderr
+  fprintf(stderr, "[hp_level] %zu levels, %d slots, cost %.2f\n", P.levels.size(), P.nslots, P.cost);
+  for (const LvLevel& L : P.levels) {
+    fprintf(stderr, "  axis %d K %d inputs %d targets %d entries %d\n", L.axis, L.K, L.nin, L.ntg,
+            (int)L.in_start[L.nin]);
+  }
+}
+
 static LvProgram plan_levels(int dim, const std::vector<Term>& terms) {
   LvProgram best;
   if (const char* e = getenv("HP_LEVEL_CUT")) {  // experiments: force the suffix/prefix cut
@@ -469,6 +478,8 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
   if (dtype != HP_C128 || (flags & HP_REF_ORDER) || s->n == 0) return HP_OK;
   LvProgram P = plan_levels(s->dim, terms);
   if (!P.ok) return HP_OK;
+  if (const char* e = getenv("HP_LEVEL_DEBUG"))
+    if (atoi(e)) dump_plan(P);
   // batches are chunked so that the intermediate vectors fit the workspace
   size_t per_vec = (size_t)std::max(P.nslots, 1) * s->n * sizeof(double2);
   int64_t chunk = std::min<int64_t>(batch, (int64_t)(ws_bytes / per_vec));
