@@ -87,6 +87,8 @@ struct AxBox {
     dn = jl > 0 ? o - stride : -1;
     up = jl < side - 1 ? o + stride : -1;
   }
+  __device__ __forceinline__ int64_t dn_of(int64_t o) const { return jloc(o) > 0 ? o - stride : -1; }
+  __device__ __forceinline__ int64_t up_of(int64_t o) const { return jloc(o) < side - 1 ? o + stride : -1; }
 };
 
 struct AxTab {
@@ -98,6 +100,8 @@ struct AxTab {
     dn = __ldg(down + o);
     up_ = __ldg(up + o);
   }
+  __device__ __forceinline__ int64_t dn_of(int64_t o) const { return __ldg(down + o); }
+  __device__ __forceinline__ int64_t up_of(int64_t o) const { return __ldg(up + o); }
 };
 
 }  // namespace hp

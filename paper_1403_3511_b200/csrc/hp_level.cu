@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <map>
+#include <mutex>
 #include <vector>
 
 #include "hp_common.cuh"
@@ -49,7 +50,7 @@ struct LvLevel {
   int nin, ntg;
   short in_buf[LV_MAXIN];   // -2 = v, >= 0 slot
   short tg_buf[LV_MAXTG];   // -1 = y, >= 0 slot
-  short in_start[LV_MAXIN + 1];
+  short ik_start[LV_MAXIN * (LV_MAXK + 1) + 1];  // entries of (input i, degree k) at [i*(K+1)+k]
   LvEnt ent[LV_MAXENT];     // grouped by input: T_0..T_K of an input are computed once
 };
 
@@ -108,16 +109,19 @@ struct Builder {
       ++L.ntg;
     }
     if ((int)all.size() > LV_MAXENT) return false;
-    std::stable_sort(all.begin(), all.end(), [](const LvEnt& a, const LvEnt& b) { return a.input < b.input; });
+    std::stable_sort(all.begin(), all.end(), [](const LvEnt& a, const LvEnt& b) {
+      return a.input != b.input ? a.input < b.input : a.k < b.k;
+    });
     int ne = 0;
-    for (int i = 0; i < L.nin; ++i) {
-      L.in_start[i] = (short)ne;
-      while (ne < (int)all.size() && all[ne].input == i) {
-        L.ent[ne] = all[ne];
-        ++ne;
+    for (int i = 0; i < L.nin; ++i)
+      for (int k = 0; k <= LV_MAXK; ++k) {
+        L.ik_start[i * (LV_MAXK + 1) + k] = (short)ne;
+        while (ne < (int)all.size() && all[ne].input == i && all[ne].k == k) {
+          L.ent[ne] = all[ne];
+          ++ne;
+        }
       }
-    }
-    L.in_start[L.nin] = (short)ne;
+    L.ik_start[L.nin * (LV_MAXK + 1)] = (short)ne;
     return true;
   }
 };
@@ -275,7 +279,7 @@ static void dump_plan(const LvProgram& P) {  // HP_LEVEL_DEBUG=1: planner output
   fprintf(stderr, "[hp_level] %zu levels, %d slots, cost %.2f\n", P.levels.size(), P.nslots, P.cost);
   for (const LvLevel& L : P.levels) {
     fprintf(stderr, "  axis %d K %d inputs %d targets %d entries %d\n", L.axis, L.K, L.nin, L.ntg,
-            (int)L.in_start[L.nin]);
+            (int)L.ik_start[L.nin * (LV_MAXK + 1)]);
   }
 }
 
@@ -315,20 +319,18 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
       }
 #pragma unroll
       for (int d = 2; d <= K; ++d) {
-        int jj;
-        int64_t a0 = -1, b0, a1, b1 = -1;
-        if (seg[K - d + 1] >= 0) ax.at(seg[K - d + 1], jj, a0, b0);
-        if (seg[K + d - 1] >= 0) ax.at(seg[K + d - 1], jj, a1, b1);
-        seg[K - d] = a0;
-        seg[K + d] = b1;
+        seg[K - d] = seg[K - d + 1] >= 0 ? ax.dn_of(seg[K - d + 1]) : -1;
+        seg[K + d] = seg[K + d - 1] >= 0 ? ax.up_of(seg[K + d - 1]) : -1;
       }
     }
-    double cd[S], cu[S];
+    // ladder coefficients of the window, sq[p] = sqrt(j_p / 2) (cd at p, cu at p - 1); positions
+    // with j < 0 are absent (forced to zero below).  Computed, not tabled: a table load would sit
+    // on the dependent chain behind the j load (measured slower on cfg3)
+    double sq[S + 1];
 #pragma unroll
-    for (int p = 0; p < S; ++p) {
-      double j = (double)(jo + p - K);
-      cd[p] = j > 0.0 ? sqrt(j * 0.5) : 0.0;
-      cu[p] = sqrt((j + 1.0) * 0.5);
+    for (int p = 0; p <= S; ++p) {
+      const int j = jo + p - K;
+      sq[p] = j > 0 ? sqrt(j * 0.5) : 0.0;
     }
     double lev = 0.0;
     if (osc)
@@ -342,12 +344,11 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
         // T_0..T_K of this input at o, once
         const int ib = lv.in_buf[ii];
         const double2* x = ib == -2 ? v + bo : slots + (int64_t)ib * n * batch + bo;
-        const int e0 = lv.in_start[ii], e1 = lv.in_start[ii + 1];
         // entries of this input at degree kk receive t (static indices only: no local memory)
         auto emit = [&](int kk, double2 t) {
+          const int e0 = lv.ik_start[ii * (LV_MAXK + 1) + kk], e1 = lv.ik_start[ii * (LV_MAXK + 1) + kk + 1];
           for (int e = e0; e < e1; ++e) {
             const LvEnt E = lv.ent[e];
-            if (E.k != kk) continue;
             if (E.tg == 0xFF) {
               slots[(int64_t)E.slot * n * batch + bo + o] = make_double2(E.w * t.x, E.w * t.y);
               continue;
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
           for (int p = k; p < S - k; ++p) {
             const double2 lo = k == 1 ? Tm[p - 1] : Tc[p - 1];
             const double2 hi = k == 1 ? Tm[p + 1] : Tc[p + 1];
-            double2 r = make_double2(sc * fma(cd[p], lo.x, cu[p] * hi.x), sc * fma(cd[p], lo.y, cu[p] * hi.y));
+            double2 r = make_double2(sc * fma(sq[p], lo.x, sq[p + 1] * hi.x), sc * fma(sq[p], lo.y, sq[p + 1] * hi.y));
             if (k > 1) {
               r.x -= Tm[p].x;
               r.y -= Tm[p].y;
