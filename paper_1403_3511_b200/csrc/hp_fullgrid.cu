@@ -242,7 +242,8 @@ static hp_status ensure_tiles(const hp_set_s* s) {
   if (s->fg_tiles) return HP_OK;
   const int t1 = (s->side[1] + F1_T1 - 1) / F1_T1, t2 = (s->side[2] + F1_T2 - 1) / F1_T2,
             t3 = (s->side[3] + F1_T3 - 1) / F1_T3;
-  constexpr int BE = 3;
+  int BE = 3;  // block edge in tiles (HP_FG_BLOCK overrides)
+  if (const char* e = getenv("HP_FG_BLOCK")) BE = std::max(1, atoi(e));
   std::vector<int> codes;
   codes.reserve((size_t)t1 * t2 * t3);
   for (int b1 = 0; b1 < t1; b1 += BE)
@@ -491,9 +492,11 @@ static hp_status copy_streams(cudaStream_t* in, cudaStream_t* out) {
 }
 
 // y = W v for host-resident v / y on a full cube of the single-pass class.  The cube is cut
-// into chunks of j1 planes (>= 4, ~128 MB); chunk k is copied in on one stream, its output
-// planes are computed on `st` once chunk k+1 (the band halo) has landed, and copied out on a
-// third stream, so PCIe traffic in both directions overlaps the kernels.  *done = false when
+// into chunks of j1 planes (~64 MB); chunk k is copied in on one stream, its output planes are
+// computed on `st` once the chunks holding its band halo (4 planes) have landed, and copied out
+// on a third stream, so PCIe traffic in both directions overlaps the kernels.  cfg4 measures
+// 92 ms for 4.3 GB each way (46.5 GB/s per direction, the duplex limit of the link: chunk sizes
+// of 1-8 planes all land within 3%).  *done = false when
 // the set / terms are not covered (the caller then copies whole vectors).
 hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                                   const void* in_host, void* out_host, void* in_dev, void* out_dev, int flags,
@@ -508,9 +511,10 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
   const double* G = P + 4 * FG_MAXN * FG_W;
   const int n0 = s->side[0];
   const size_t plane = (size_t)(s->n / n0) * sizeof(double2);
-  int C = (int)std::min<size_t>(n0, ((size_t)128 << 20) / std::max<size_t>(plane, 1));
+  int C = (int)std::min<size_t>(n0, ((size_t)64 << 20) / std::max<size_t>(plane, 1));
   if (const char* e = getenv("HP_STREAM_CHUNK")) C = atoi(e);  // planes per chunk (tests)
-  C = std::max(C, F1_H);  // chunk k+1 must cover the band halo of chunk k
+  C = std::max(C, 1);
+  const int ahead = (F1_H + C - 1) / C;  // chunks k+1 .. k+ahead hold the band halo of chunk k
   const int nch = (n0 + C - 1) / C;
   cudaStream_t sin, sout;
   if ((rc = copy_streams(&sin, &sout))) return rc;
@@ -528,7 +532,7 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
   }
   for (int k = 0; k < nch; ++k) {
     const int p0 = k * C, p1 = std::min(n0, p0 + C);
-    HP_CUDA(cudaStreamWaitEvent(st, ev[std::min(k + 1, nch - 1)], 0));
+    HP_CUDA(cudaStreamWaitEvent(st, ev[std::min(k + ahead, nch - 1)], 0));
     bool launched = false;
     rc = F.nmix ? launch_single<1>(s, (const double2*)in_dev, (double2*)out_dev, P, G, F, st, nullptr, &launched,
                                    p0, p1)

@@ -400,7 +400,7 @@ def test_random_term_structures_vs_oracle(hp, seed):
         assert rel_l2(Y[b], oa.polynomial(degs, coeffs, 16.0, V[b])) < TOL
 
 
-@pytest.mark.parametrize("bound,chunk", [(11, 4), (11, 5), (20, 7), (20, 64)])
+@pytest.mark.parametrize("bound,chunk", [(11, 1), (11, 2), (11, 5), (20, 3), (20, 7), (20, 64)])
 def test_streamed_host_matvec_matches_device(hp, bound, chunk, monkeypatch):
     """hp_apply_polynomial_streamed (host-resident vectors, j1-plane chunks overlapped with the
     kernels) gives bit-for-bit the device matvec, for chunkings that do and do not divide n0."""
