@@ -175,7 +175,16 @@ struct AllTab {
 static int g_blocks(int64_t n) { return grid_for(n, 256, 148 * 16); }
 
 // workspace cap per call of the generic program; batches beyond it are chunked
-static const size_t kChunkCap = (size_t)24 << 30;
+// batched workspaces are capped (HP_CHUNK_GB overrides, GiB): larger chunks let the level
+// kernels share each point's line walk across more vectors of the batch
+static size_t chunk_cap() {
+  static size_t v = [] {
+    const char* e = getenv("HP_CHUNK_GB");
+    return (size_t)(e ? std::max(1, atoi(e)) : 24) << 30;
+  }();
+  return v;
+}
+#define kChunkCap chunk_cap()
 
 template <class T>
 static hp_status launch_cheb(const hp_set_s* s, int a, int mode, double scale, const T* w, const T* wm,
