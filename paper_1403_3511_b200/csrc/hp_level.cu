@@ -23,6 +23,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <map>
+#include <memory>
+#include <mutex>
+#include <string>
 #include <mutex>
 #include <vector>
 
@@ -296,6 +299,25 @@ static LvProgram plan_levels(int dim, const std::vector<Term>& terms) {
   return best;
 }
 
+// plans are cached per (dim, term list): the planner tries every cut with map-heavy builders,
+// which is tens of microseconds of host time per call -- the whole budget of a small matvec
+static std::shared_ptr<const LvProgram> cached_plan(int dim, const std::vector<Term>& terms) {
+  static std::mutex mtx;
+  static std::map<std::string, std::shared_ptr<const LvProgram>> cache;
+  std::string key((const char*)&dim, sizeof(int));
+  for (const Term& t : terms) {
+    key.append((const char*)t.r, sizeof(int) * dim);
+    key.append((const char*)&t.alpha, sizeof(double));
+  }
+  std::lock_guard<std::mutex> g(mtx);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cache.size() > 256) cache.clear();  // time-dependent surrogates: bounded
+  auto P = std::make_shared<const LvProgram>(plan_levels(dim, terms));
+  cache.emplace(key, P);
+  return P;
+}
+
 // ---------------------------------------------------------------- kernel
 
 template <int K, int TGN, class AX, class AXS>
@@ -466,7 +488,8 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
 
 size_t level_workspace_bytes(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch) {
   if (dtype != HP_C128) return 0;
-  LvProgram P = plan_levels(s->dim, terms);
+  const auto Pp = cached_plan(s->dim, terms);
+  const LvProgram& P = *Pp;
   if (!P.ok) return 0;
   return (size_t)std::max(P.nslots, 1) * s->n * batch * sizeof(double2);
 }
@@ -477,7 +500,8 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
   *done = false;
   if (dot) dot->n = 0;
   if (dtype != HP_C128 || (flags & HP_REF_ORDER) || s->n == 0) return HP_OK;
-  LvProgram P = plan_levels(s->dim, terms);
+  const auto Pp = cached_plan(s->dim, terms);
+  const LvProgram& P = *Pp;
   if (!P.ok) return HP_OK;
   if (const char* e = getenv("HP_LEVEL_DEBUG"))
     if (atoi(e)) dump_plan(P);
