@@ -89,6 +89,14 @@ struct AxBox {
   }
   __device__ __forceinline__ int64_t dn_of(int64_t o) const { return jloc(o) > 0 ? o - stride : -1; }
   __device__ __forceinline__ int64_t up_of(int64_t o) const { return jloc(o) < side - 1 ? o + stride : -1; }
+  // the axis line through o out to +-K: seg[K + d] = ordinal of j + d e, or -1 (one division)
+  template <int K>
+  __device__ __forceinline__ void segment(int64_t o, int& j, int64_t* seg) const {
+    const int jl = o < (int64_t)0x7fffffff ? (int)(((unsigned)o / (unsigned)stride) % (unsigned)side) : jloc(o);
+    j = jl + joff;
+#pragma unroll
+    for (int d = -K; d <= K; ++d) seg[K + d] = (jl + d >= 0 && jl + d < side) ? o + d * stride : -1;
+  }
 };
 
 struct AxTab {
@@ -102,6 +110,23 @@ struct AxTab {
   }
   __device__ __forceinline__ int64_t dn_of(int64_t o) const { return __ldg(down + o); }
   __device__ __forceinline__ int64_t up_of(int64_t o) const { return __ldg(up + o); }
+  // the axis line through o out to +-K via the tables (down chains never break in a
+  // downward-closed set; up chains stop at the first pruned index)
+  template <int K>
+  __device__ __forceinline__ void segment(int64_t o, int& j, int64_t* seg) const {
+    int64_t dn, up_;
+    at(o, j, dn, up_);
+    seg[K] = o;
+    if (K > 0) {
+      seg[K - 1] = dn;
+      seg[K + 1] = up_;
+    }
+#pragma unroll
+    for (int d = 2; d <= K; ++d) {
+      seg[K - d] = seg[K - d + 1] >= 0 ? dn_of(seg[K - d + 1]) : -1;
+      seg[K + d] = seg[K + d - 1] >= 0 ? up_of(seg[K + d - 1]) : -1;
+    }
+  }
 };
 
 }  // namespace hp

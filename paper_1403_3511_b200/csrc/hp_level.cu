@@ -331,20 +331,7 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
     // the axis line through o: seg[K + d] = ordinal of j + d e_a, or -1
     int64_t seg[S];
     int jo;
-    {
-      int64_t dn, up;
-      ax.at(o, jo, dn, up);
-      seg[K] = o;
-      if (K > 0) {
-        seg[K - 1] = dn;
-        seg[K + 1] = up;
-      }
-#pragma unroll
-      for (int d = 2; d <= K; ++d) {
-        seg[K - d] = seg[K - d + 1] >= 0 ? ax.dn_of(seg[K - d + 1]) : -1;
-        seg[K + d] = seg[K + d - 1] >= 0 ? ax.up_of(seg[K + d - 1]) : -1;
-      }
-    }
+    ax.template segment<K>(o, jo, seg);
     // ladder coefficients of the window, sq[p] = sqrt(j_p / 2) (cd at p, cu at p - 1); positions
     // with j < 0 are absent (forced to zero below).  Computed, not tabled: a table load would sit
     // on the dependent chain behind the j load (measured slower on cfg3)
