@@ -440,3 +440,29 @@ def test_streamed_host_matvec_fallback_sets(hp):
         appl.apply_host_into(ap, xh, yh)
         torch.cuda.synchronize()
         assert np.array_equal(yh.numpy(), appl.apply_polynomial(ap, v))
+
+
+def test_streamed_host_matvec_batch_and_flags(hp):
+    """Batched vectors and the reference-order flag take the whole-copy route of the streamed
+    entry point: results equal the device calls bit for bit."""
+    import torch
+
+    w = W.CONFIGS["cfg4"].scaled(7, "cfg4x")
+    ap = w.approx(0.3)
+    s = hp.build_full(w.dim, w.bound)
+    appl = hp.get_applier(s)
+    gen = np.random.default_rng(11)
+    V = gen.standard_normal((2, s.size)) + 1j * gen.standard_normal((2, s.size))
+    xh = torch.from_numpy(V).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    appl.apply_host_into(ap, xh, yh)
+    torch.cuda.synchronize()
+    assert np.array_equal(yh.numpy(), appl.apply_polynomial(ap, V))
+    v = V[0].copy()
+    xh1 = torch.from_numpy(v).pin_memory()
+    yh1 = torch.empty_like(xh1).pin_memory()
+    appl.apply_host_into(ap, xh1, yh1, 2)  # HP_REF_ORDER
+    torch.cuda.synchronize()
+    assert np.array_equal(yh1.numpy(), appl.apply_polynomial(ap, v, ref_order=True))
+    with pytest.raises(ValueError):
+        appl.apply_host_into(ap, xh1.cuda(), yh1)
