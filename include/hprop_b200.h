@@ -138,6 +138,18 @@ hp_status hp_apply_polynomial_streamed(hp_set_t s, const int32_t* degrees_host, 
                                        int flags, void* workspace_dev, size_t workspace_bytes,
                                        void* stream);
 
+/* apply_polynomial restricted to the output j1-planes [plane_lo, plane_hi) of a full cube or
+ * slab (plane indices local to the set).  Only input planes plane_lo-4 .. plane_hi+3 are read
+ * (4 = the band radius of the fused evaluator), so a slab-sharded matvec can compute the
+ * planes that need no halo while the halo planes are in flight; the other
+ * output planes are not written.  HP_ERR_VALUE outside the fused full-cube class (complex
+ * vectors, batch 1, even single-axis bands, at most one x1*x2-type coupling); an empty range
+ * only answers that question. */
+hp_status hp_apply_polynomial_planes(hp_set_t s, const int32_t* degrees_host, const double* coeffs_host,
+                                     int nterms, double halfwidth, int dtype, const void* in_dev,
+                                     void* out_dev, int plane_lo, int plane_hi, int flags,
+                                     void* workspace_dev, size_t workspace_bytes, void* stream);
+
 /* apply_square_sum -- fast_apply.py:202-245 (exact restricted sum_l x_l^2) */
 hp_status hp_square_sum(hp_set_t s, int dtype, const void* in_dev, void* out_dev,
                         int64_t batch, void* stream);

@@ -56,6 +56,8 @@ SIGNATURES = {
                                     c_i32p, c_vp, c_sz, c_vp]),
     "hp_apply_polynomial_streamed": (c_int, [c_vp, c_i32p, c_dblp, c_int, c_dbl, c_int, c_vp, c_vp, c_vp, c_vp,
                                              c_i64, c_int, c_vp, c_sz, c_vp]),
+    "hp_apply_polynomial_planes": (c_int, [c_vp, c_i32p, c_dblp, c_int, c_dbl, c_int, c_vp, c_vp, c_int, c_int,
+                                           c_int, c_vp, c_sz, c_vp]),
     "hp_square_sum": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_vp]),
     "hp_magnus_workspace_bytes": (c_sz, [c_vp, c_int, c_i32p, c_int, c_i32p, c_int, c_int]),
     "hp_magnus_step": (c_int, [c_vp, c_int, c_i32p, c_dblp, c_int, c_i32p, c_dblp, c_int, c_dbl, c_dbl,
@@ -110,6 +112,10 @@ def load(require_device: bool = True):
 
 def lib():
     return load(True)
+
+
+def last_error() -> str:
+    return _lib.hp_last_error().decode() if _lib is not None else ""
 
 
 def check(status: int) -> None:

@@ -470,6 +470,33 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
 }
 
 
+// ---------------------------------------------------------------- plane ranges
+
+// y on output j1-planes [plo, phi) only (reads input planes [plo - 4, phi + 4)); *done = false
+// when the set / terms are outside the single-pass class
+hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
+                                const void* in, void* out, int plo, int phi, int flags, void* ws, size_t ws_bytes,
+                                cudaStream_t st, bool* done) {
+  *done = false;
+  FgPlan F = classify(s, terms, dtype, 1, flags);
+  if (!F.ok || !fg_single_class(F)) return HP_OK;
+  if (plo == phi) {  // support query: nothing to compute
+    *done = ws_bytes >= fullgrid_workspace_bytes(s, terms, dtype, 1, flags);
+    return HP_OK;
+  }
+  bool ok = false;
+  hp_status rc = fg_prepare(s, terms, halfwidth, dtype, 1, flags, ws, ws_bytes, st, &F, &ok);
+  if (rc || !ok) return rc;
+  const double* P = (const double*)ws;
+  const double* G = P + 4 * FG_MAXN * FG_W;
+  bool launched = false;
+  rc = F.nmix ? launch_single<1>(s, (const double2*)in, (double2*)out, P, G, F, st, nullptr, &launched, plo, phi)
+              : launch_single<0>(s, (const double2*)in, (double2*)out, P, G, F, st, nullptr, &launched, plo, phi);
+  if (rc) return rc;
+  *done = launched;
+  return HP_OK;
+}
+
 // ---------------------------------------------------------------- streamed (host-resident vectors)
 
 // copy streams of the streamed matvec, one pair per device

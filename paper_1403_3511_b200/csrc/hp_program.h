@@ -77,6 +77,9 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
                          const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
                          cudaStream_t st, bool* done, DotOut* dot = nullptr);
 
+hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
+                                const void* in, void* out, int plo, int phi, int flags, void* ws, size_t ws_bytes,
+                                cudaStream_t st, bool* done);
 hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                                   const void* in_host, void* out_host, void* in_dev, void* out_dev, int flags,
                                   void* ws, size_t ws_bytes, cudaStream_t st, bool* done);

@@ -181,6 +181,41 @@ class PolynomialApplier:
             float(approx.halfwidth), dtype, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), batch,
             flags, None, ctypes.c_void_p(ws.data_ptr()), ws.numel(), nat.stream_ptr()))
 
+    def apply_planes_into(self, approx, x, y, plane_lo: int, plane_hi: int, flags: int = 0) -> bool:
+        """y <- W(X) x on the output j1-planes [plane_lo, plane_hi) of a full cube / slab only.
+
+        Reads input planes plane_lo - 4 .. plane_hi + 3 (hp_apply_polynomial_planes).  Returns
+        False (nothing launched) when the surrogate is outside the fused full-cube class; the
+        answer is cached per (approx, flags).
+        """
+        import torch
+
+        key = (id(approx), tuple(x.shape), x.dtype, flags)
+        cache = self.__dict__.setdefault("_into_cache", {})
+        ent = cache.get(key)
+        if ent is None:
+            degs, coeffs = _term_arrays(approx, self.iset.dim)
+            dtype = nat.HP_C128 if x.is_complex() else nat.HP_F64
+            h = ctypes.c_void_p(self.iset.handle)
+            wsb = nat.lib().hp_poly_workspace_bytes(h, degs.ctypes.data_as(nat.c_i32p), degs.shape[0], dtype, 1,
+                                                    flags)
+            ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=x.device)
+            ent = (approx, degs, coeffs, h, 1, dtype, ws)
+            cache[key] = ent
+        _, degs, coeffs, h, _batch, dtype, ws = ent
+        unsupported = self.__dict__.setdefault("_planes_unsupported", set())
+        if key in unsupported:
+            return False
+        st = nat.lib().hp_apply_polynomial_planes(
+            h, degs.ctypes.data_as(nat.c_i32p), coeffs.ctypes.data_as(nat.c_dblp), degs.shape[0],
+            float(approx.halfwidth), dtype, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+            int(plane_lo), int(plane_hi), flags, ctypes.c_void_p(ws.data_ptr()), ws.numel(), nat.stream_ptr())
+        if st == nat.HP_ERR_VALUE and "fused full-cube" in nat.last_error():
+            unsupported.add(key)
+            return False
+        nat.check(st)
+        return True
+
     def apply_host_into(self, approx, x_host, y_host, flags: int = 0) -> None:
         """Host-resident vectors: y_host <- W(X) x_host for CPU tensors (pin them for overlap).
 

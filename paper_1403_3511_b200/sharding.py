@@ -18,6 +18,9 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+# input planes the fused full-cube kernel reads on each side of an output plane (hp_fg1.cuh F1_H)
+RADIUS = 4
+
 
 def partition(planes: int, world: int, rank: int) -> tuple[int, int]:
     """Near-equal contiguous split of `planes` j1-planes over `world` ranks."""
@@ -133,7 +136,40 @@ class SlabShard:
         g = self.geo
         return c[g.blo * g.plane:g.bhi * g.plane].copy()
 
-    def apply_polynomial(self, appl, ap, x, y, flags: int = 0):
-        """y[own] = W(X) x on this rank's planes; x, y are box-sized device tensors."""
-        halo_exchange(self.geo, x)
-        appl.apply_into(ap, x, y, flags)
+    def interior(self) -> tuple[int, int] | None:
+        """Local output planes whose inputs are all owned (the fused kernel reads +-4 planes):
+        computable while the halo planes are in flight.  None when there are none."""
+        g = self.geo
+        lo, hi = g.lo - g.blo, g.hi - g.blo
+        ilo = lo + (RADIUS if g.rank > 0 else 0)
+        ihi = hi - (RADIUS if g.rank < g.world - 1 else 0)
+        return (ilo, ihi) if ihi > ilo else None
+
+    def apply_polynomial(self, appl, ap, x, y, flags: int = 0, overlap: bool = True, exchange=None):
+        """y[own] = W(X) x on this rank's planes; x, y are box-sized device tensors.
+
+        With `overlap`, the halo exchange runs on a side stream while the interior planes are
+        computed (hp_apply_polynomial_planes), then the boundary planes; otherwise exchange,
+        then one matvec over the box.  `exchange(geo, x)` replaces halo_exchange (tests).
+        """
+        import torch
+
+        exch = exchange or halo_exchange
+        rng = self.interior() if overlap and self.geo.world > 1 else None
+        if rng is None or not appl.apply_planes_into(ap, x, y, rng[0], rng[0], flags):
+            exch(self.geo, x)
+            appl.apply_into(ap, x, y, flags)
+            return
+        g = self.geo
+        lo, hi = g.lo - g.blo, g.hi - g.blo
+        main = torch.cuda.current_stream()
+        side = self.__dict__.setdefault("_side", torch.cuda.Stream())
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            exch(g, x)  # NCCL on the side stream
+        appl.apply_planes_into(ap, x, y, rng[0], rng[1], flags)  # reads owned planes only
+        main.wait_stream(side)
+        if rng[0] > lo:
+            appl.apply_planes_into(ap, x, y, lo, rng[0], flags)
+        if hi > rng[1]:
+            appl.apply_planes_into(ap, x, y, rng[1], hi, flags)
