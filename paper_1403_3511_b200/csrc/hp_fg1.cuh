@@ -2,29 +2,37 @@
 //
 // y = [c0 + sum_a P_a(X_a) + T_r0(X_0) G(X_1)] v on a 4-D box, ONE read of v and
 // ONE write of y per coefficient (32 B algorithmic), instead of the two HBM
-// passes of k_fg_inner2 / k_fg_outer3 (80 B).
+// passes of k_fg_inner2 / k_fg_outer3 (80 B).  (Axes 0-based here: axis 0 is
+// DESIGN.md's j1.)
 //
-// Work decomposition.  The cross-section (j1, j2, j3) is cut into 8x8x8
-// tiles; one persistent CTA per SM (512 threads, one point of the tile per
-// thread) takes tiles in a blocked order and marches axis 0 through all n0
-// planes of its tile.  For every plane p, one elected thread issues five TMA
-// boxes into a pipeline stage: the tile with its +-4 rows along j1 (axis-1
-// stencil and the G coupling), and the +-4 halos along j2 and j3.  Boxes that
-// run off the cube are zero-filled by the TMA unit, which is exactly the
-// truncation of the ladder operators at the box faces.  Halo planes of the
-// neighbouring tiles were fetched from HBM by the CTAs that own them a few
-// planes earlier (all 148 CTAs march at the same rate over a compact block
-// of tiles), so they come from L2.
+// Work decomposition.  The cross-section (j1, j2, j3) is cut into 8x4x16
+// tiles (512 points); one persistent 256-thread CTA per SM takes tiles in a
+// blocked order (ensure_tiles) and marches axis 0 through the n0 planes of its
+// tile.  For every plane p one elected thread issues three TMA boxes into one
+// of F1_S pipeline stages (40 KB): the tile with its +-4 rows along j1 (axis-1
+// stencil and the G coupling) and +-4 columns along j3 (384 B rows: 64 B halo
+// rows cost the TMA unit twice as much per byte), and the +-4 rows along j2.
+// Boxes that run off the cube are zero-filled by the TMA unit -- exactly the
+// truncation of the ladder operators at the box faces.  Halo rows of the
+// neighbouring tiles were fetched from HBM by the CTAs that own them at about
+// the same time, so they mostly come from L2.  Each stage has a "full"
+// mbarrier (transaction bytes) and an "empty" one (one arrival per warp).
 //
 // Axis 0 is the march axis: instead of a 9-plane window of v, each thread
 // keeps a 9-slot ring of PARTIAL OUTPUTS y(p-4 .. p+4) in registers.  When
 // plane p arrives it scatters c = v(p) into y(p + d) with the band weight
-// P_0(p + d, -d) (uniform over the CTA), adds the in-plane stencil of axes
-// 1-3 and scatters g = G v(p) through T_r0(X_0); y(p-4) is then complete and
-// is stored.  Ring slots are compile-time (march unrolled by 9).
+// P_0(p + d, -d) (a per-plane row staged in smem, uniform over the CTA), adds
+// the in-plane stencil of axes 1-3 and scatters g = G v(p) through T_r0(X_0);
+// y(p-4) is then complete and is stored.  Ring slots are compile-time (march
+// unrolled by 9).  With NP = 2 a thread owns rows j1 and j1 + 2 of the tile,
+// whose axis-1 and coupling taps overlap (9 shared loads instead of 14).
 //
-// Weights: the in-plane band rows of the thread's (j1, j2, j3) are loaded once
-// per tile into registers; the axis-0 rows are broadcast loads per plane.
+// Bounds: the shared-memory port (TMA fills + stencil reads)
+// and L2->SM traffic; the kernel runs at 62-66% of the smem-port floor.  A
+// plane range [plo, phi) restricts the output planes (streamed host vectors,
+// overlapped slab shards).  `exp` bits are timing instrumentation only
+// (HP_FG_EXP: 1 skip halo boxes, 2 pipeline only, 8 compute only, 16-48 L2
+// policy), all off in production.
 #pragma once
 
 #include <cuda.h>
