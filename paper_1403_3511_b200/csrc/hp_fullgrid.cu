@@ -1,4 +1,9 @@
-// Fused full-cube evaluator for N = 4 boxes (cfg4 class), two HBM passes.
+// Fused full-cube evaluator for N = 4 boxes (cfg4 class).
+//
+// The even-band class (all single-axis bands even, at most one r1 = 1 coupling on axes
+// (1, 2)) runs the single-pass TMA kernel of hp_fg1.cuh (one HBM read of v, one write of y);
+// every other covered structure runs the two-pass split below.  Both share the band tables
+// and the term classification.
 //
 // On a full cube (or a j1-slab of one) the restricted ladders of different
 // axes commute, so every term alpha_r prod_l T_{r_l}(X_l/L) is a tensor
