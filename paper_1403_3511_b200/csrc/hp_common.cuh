@@ -159,6 +159,9 @@ struct hp_set_s {
   // single-pass evaluator: blocked tile order (packed i1 | i2 << 10 | i3 << 20)
   mutable int* fg_tiles = nullptr;
   mutable int fg_ntiles = 0;
+  // the same for the quad kernel's 8 x 8 x 16 tiles (hp_fg4.cuh)
+  mutable int* fg_tiles4 = nullptr;
+  mutable int fg_ntiles4 = 0;
 
   hp::AxBox box(int a) const {
     hp::AxBox v;

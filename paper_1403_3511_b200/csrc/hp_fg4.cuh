@@ -1,0 +1,414 @@
+// Single-pass fused full-cube evaluator, quad variant: 1024-point tiles, four points per thread.
+//
+// Same operator and march as k_fg_single (hp_fg1.cuh):
+//   y = [c0 + sum_a P_a(X_a) + T_r0(X_0) G(X_1)] v  on a 4-D box (axes 0-based, axis 0 = j1),
+// one read of v and one write of y per coefficient.  What changes is the per-SM working set:
+//
+// * Tiles are 8 x 8 x 16 (axes 1, 2, 3) = 1024 points instead of 512, so the halo staged per
+//   plane falls from 5x to 4x the tile (64 B/coef of TMA fills instead of 80): box A1 =
+//   [axis 1 +-4][axis 2][axis 3 +-4] (384 B rows), boxes B2 = the +-4 rows along axis 2.
+// * Each thread owns the 2 x 2 points {a, a+2} x {b, b+2} (axes 1, 2) of one axis-3 column.
+//   Even-offset taps of the pair overlap along both axes: 42 shared-memory loads serve the four
+//   points' 84 taps (10.5 per point instead of 12.5).
+// * The march-axis ring of partial outputs has 8 slots instead of 9: at step p the slot of
+//   y(p-4) receives its last term (from v(p)), is stored, and is reused for y(p+4).
+//
+// Shared-memory port budget per coefficient (the bound of this class of kernel):
+// 64 B fills + 168 B loads, against 80 + 200 for k_fg_single.
+#pragma once
+
+#ifndef Q_FENCES
+#define Q_FENCES 1
+#endif
+#if Q_FENCES
+#define Q_FENCE() asm volatile("" ::: "memory")
+#else
+#define Q_FENCE() \
+  do {            \
+  } while (0)
+#endif
+
+namespace hp {
+
+constexpr int Q_T1 = 8, Q_T2 = 8, Q_T3 = 16;
+constexpr int Q_H = FG_K;
+constexpr int Q_NT = 256;
+constexpr int Q_POINTS = Q_T1 * Q_T2 * Q_T3;
+constexpr int Q_RW = Q_T3 + 2 * Q_H;                 // A1 row (axis 3) length: 24
+constexpr int Q_R1 = Q_T2 * Q_RW;                    // A1 axis-1 stride: 192
+constexpr int Q_A1 = (Q_T1 + 2 * Q_H) * Q_R1;        // 3072
+constexpr int Q_B2R1 = Q_H * Q_T3;                   // B2 axis-1 stride: 64
+constexpr int Q_B2 = Q_T1 * Q_B2R1;                  // 512
+constexpr int Q_OFF_LO = Q_A1, Q_OFF_HI = Q_A1 + Q_B2;
+constexpr int Q_STAGE = Q_A1 + 2 * Q_B2;             // 4096 double2 = 64 KB
+constexpr unsigned Q_STAGE_BYTES = Q_STAGE * 16u;
+#ifndef Q_STAGES
+#define Q_STAGES 3
+#endif
+constexpr int Q_S = Q_STAGES;
+constexpr size_t Q_WOFF = (size_t)Q_S * Q_STAGE_BYTES;
+constexpr int Q_T1W = 8;  // doubles per axis-1 weight row
+constexpr int Q_MAXN = 128;  // largest side the shared tables are sized for (larger cubes: k_fg_single)
+constexpr size_t Q_TOFF = Q_WOFF + (size_t)Q_MAXN * F1_WROW * sizeof(double);
+constexpr size_t Q_T2OFF = Q_TOFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
+constexpr size_t Q_T3OFF = Q_T2OFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
+constexpr int Q_T3N = Q_MAXN + 16;  // axis-3 table: [5][Q_T3N], transposed (16 lanes read 128 B)
+constexpr size_t Q_BOFF = Q_T3OFF + (size_t)5 * Q_T3N * sizeof(double);
+constexpr size_t Q_SMEM = Q_BOFF + 2 * Q_S * sizeof(uint64_t) + 8 * sizeof(int);
+
+__device__ __forceinline__ void q_prefetch4(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(
+                   (unsigned long long)m),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+
+template <int NMIX, bool DOT>
+__global__ void __launch_bounds__(Q_NT, 1)
+    k_fg_quad(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB2,
+              const double2* __restrict__ v, double2* __restrict__ y, const double* __restrict__ P,
+              const double* __restrict__ G, const double* __restrict__ B0, const int* __restrict__ tiles, int ntiles,
+              int n0, int n1, int n2, int n3, double2* __restrict__ dotp, int exp, int plo, int phi) {
+  extern __shared__ __align__(128) unsigned char q_smem[];
+  double2* stg = (double2*)q_smem;
+  double* W = (double*)(q_smem + Q_WOFF);
+  double* T1w = (double*)(q_smem + Q_TOFF);
+  double* T2w = (double*)(q_smem + Q_T2OFF);
+  double* T3w = (double*)(q_smem + Q_T3OFF);
+  uint64_t* full = (uint64_t*)(q_smem + Q_BOFF);
+  uint64_t* empty = full + Q_S;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int c = tid & 15, bq = (tid >> 4) & 3, aq = tid >> 6;
+  const int a = (aq >> 1) * 4 + (aq & 1), b = (bq >> 1) * 4 + (bq & 1);
+  const double* P0 = P;
+  const double* P1 = P + FG_MAXN * FG_W;
+  const double* P2 = P + 2 * FG_MAXN * FG_W;
+  const double* P3 = P + 3 * FG_MAXN * FG_W;
+  if (tid == 0) {
+    for (int s = 0; s < Q_S; ++s) {
+      f1_mbar_init(&full[s], 1);
+      f1_mbar_init(&empty[s], Q_NT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // per-plane scatter weights (k_fg_single's row layout):
+  // {P0(p,0), P0(p+2,-2), P0(p-2,2), P0(p+4,-4), P0(p-4,4), B0(p+1,-1), B0(p-1,1), 0}
+  for (int q = tid; q < n0; q += Q_NT) {
+    auto p0 = [&](int r, int e) { return (r >= 0 && r < n0) ? P0[r * FG_W + e + FG_K] : 0.0; };
+    auto b0 = [&](int r, int e) { return (NMIX && r >= 0 && r < n0) ? B0[r * FG_W + e + FG_K] : 0.0; };
+    double* w = W + q * F1_WROW;
+    w[0] = p0(q, 0);
+    w[1] = p0(q + 2, -2);
+    w[2] = p0(q - 2, 2);
+    w[3] = p0(q + 4, -4);
+    w[4] = p0(q - 4, 4);
+    w[5] = b0(q + 1, -1);
+    w[6] = b0(q - 1, 1);
+    w[7] = 0.0;
+  }
+  // axis-1 rows r = 0 .. n1+7: {P1(r,-4), P1(r,-2), P1(r,2), P1(r,4), G(r,-1), G(r,+1), P1(r,0), 0}
+  // (rows past the cube are zeros: their points are never stored)
+  for (int r = tid; r < n1 + 8; r += Q_NT) {
+    double* w = T1w + r * Q_T1W;
+    const bool ok = r < n1;
+    w[0] = ok ? P1[r * FG_W + FG_K - 4] : 0.0;
+    w[1] = ok ? P1[r * FG_W + FG_K - 2] : 0.0;
+    w[2] = ok ? P1[r * FG_W + FG_K + 2] : 0.0;
+    w[3] = ok ? P1[r * FG_W + FG_K + 4] : 0.0;
+    w[4] = ok && NMIX ? G[r * FG_W + FG_K - 1] : 0.0;
+    w[5] = ok && NMIX ? G[r * FG_W + FG_K + 1] : 0.0;
+    w[6] = ok ? P1[r * FG_W + FG_K] : 0.0;
+    w[7] = 0.0;
+  }
+  // axis-2 rows: {P2(r,-4), P2(r,-2), P2(r,2), P2(r,4), P2(r,0), 0, 0, 0}
+  for (int r = tid; r < n2 + 8; r += Q_NT) {
+    double* w = T2w + r * Q_T1W;
+    const bool ok = r < n2;
+    w[0] = ok ? P2[r * FG_W + FG_K - 4] : 0.0;
+    w[1] = ok ? P2[r * FG_W + FG_K - 2] : 0.0;
+    w[2] = ok ? P2[r * FG_W + FG_K + 2] : 0.0;
+    w[3] = ok ? P2[r * FG_W + FG_K + 4] : 0.0;
+    w[4] = ok ? P2[r * FG_W + FG_K] : 0.0;
+    w[5] = w[6] = w[7] = 0.0;
+  }
+  // axis-3 columns, transposed: T3w[i][r] = P3(r, -4, -2, 2, 4, 0 for i = 0..4)
+  for (int r = tid; r < Q_T3N; r += Q_NT) {
+    const bool ok = r < n3;
+    T3w[0 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K - 4] : 0.0;
+    T3w[1 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K - 2] : 0.0;
+    T3w[2 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K + 2] : 0.0;
+    T3w[3 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K + 4] : 0.0;
+    T3w[4 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K] : 0.0;
+  }
+  __syncthreads();
+
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int ps0 = max(plo - Q_H, 0), pe = min(phi + Q_H, n0), nper = pe - ps0;
+  const int nitems = my_tiles * nper;
+  int* ps_ = (int*)(empty + Q_S);
+  if (tid == 0) {
+    for (int i = 0; i < 8; ++i) ps_[i] = 0;
+    ps_[2] = ps0;
+  }
+  auto issue_next = [&]() {
+    int pk = ps_[0], pti = ps_[1], pp = ps_[2], ps = ps_[3], pu = ps_[4];
+    if (pk >= nitems) return;
+    if (pu > 0) f1_mbar_wait(&empty[ps], (unsigned)((pu - 1) & 1));
+    if (pp == ps0) {
+      const int code = __ldg(tiles + blockIdx.x + pti * gridDim.x);
+      ps_[5] = (code & 1023) * Q_T1;
+      ps_[6] = ((code >> 10) & 1023) * Q_T2;
+      ps_[7] = (code >> 20) * Q_T3;
+    }
+    const int T1 = ps_[5], T2 = ps_[6], T3 = ps_[7];
+    double2* dst = stg + (size_t)ps * Q_STAGE;
+    uint64_t* bar = &full[ps];
+    f1_mbar_expect(bar, Q_STAGE_BYTES);
+    const uint64_t pol = f1_policy(2);
+    f1_tma4_hint(dst, &mA1, 2 * (T3 - Q_H), T2, T1 - Q_H, pp, bar, pol);
+    f1_tma4_hint(dst + Q_OFF_LO, &mB2, 2 * T3, T2 - Q_H, T1, pp, bar, pol);
+    f1_tma4_hint(dst + Q_OFF_HI, &mB2, 2 * T3, T2 + Q_T2, T1, pp, bar, pol);
+    // L2 prefetch of the same boxes PD planes ahead (HP_FG_EXP bits 8-15; 0 = off): turns the
+    // TMA fills of later planes into L2 hits
+    const int PD = (exp >> 8) & 255;
+    if (PD && pp + PD < pe) {
+      q_prefetch4(&mA1, 2 * (T3 - Q_H), T2, T1 - Q_H, pp + PD);
+      q_prefetch4(&mB2, 2 * T3, T2 - Q_H, T1, pp + PD);
+      q_prefetch4(&mB2, 2 * T3, T2 + Q_T2, T1, pp + PD);
+    }
+    ++pk;
+    if (++pp == pe) {
+      pp = ps0;
+      ++pti;
+    }
+    if (++ps == Q_S) {
+      ps = 0;
+      ++pu;
+    }
+    ps_[0] = pk;
+    ps_[1] = pti;
+    ps_[2] = pp;
+    ps_[3] = ps;
+    ps_[4] = pu;
+  };
+  if (tid == 0)
+    for (int k = 0; k < Q_S - 1; ++k) issue_next();
+
+  // centre of point (a, b) in A1; the other three points are +2 rows along axes 1 / 2
+  const int oc = (a + Q_H) * Q_R1 + b * Q_RW + c + Q_H;
+  // axis-2 taps of row r (= a or a + 2) at axis-2 index t: A1 inside the tile, B2 boxes outside
+  auto o2 = [&](int r, int t) {
+    return t < 0 ? Q_OFF_LO + r * Q_B2R1 + (t + Q_H) * Q_T3 + c
+                 : (t >= Q_T2 ? Q_OFF_HI + r * Q_B2R1 + (t - Q_T2) * Q_T3 + c : (r + Q_H) * Q_R1 + t * Q_RW + c + Q_H);
+  };
+  // per thread, fixed over the whole run: t = b-4, b-2, b+4, b+6 for rows a and a+2
+  // (row a + 2 = row a + 2 axis-1 strides: 2 Q_R1 in A1, 2 Q_B2R1 in the B2 boxes)
+  int o2a[4];
+  {
+    const int ts[4] = {b - 4, b - 2, b + 4, b + 6};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o2a[i] = o2(a, ts[i]);
+  }
+  const int dlo = b < Q_H ? 2 * Q_B2R1 : 2 * Q_R1;  // taps b-4, b-2: B2 box iff b < 4
+  const int dhi = b < Q_H ? 2 * Q_R1 : 2 * Q_B2R1;  // taps b+4, b+6: B2 box iff b >= 4
+
+  double2 dacc = make_double2(0.0, 0.0);
+  int cs = 0, cu = 0;
+  const int64_t plane = (int64_t)n1 * n2 * n3;
+  const int s1 = 2 * n2 * n3, s2 = 2 * n3;  // global offsets of the +2 rows along axes 1, 2
+  for (int ti = 0; ti < my_tiles; ++ti) {
+    const int code = __ldg(tiles + blockIdx.x + ti * gridDim.x);
+    const int J1 = (code & 1023) * Q_T1 + a, J2 = ((code >> 10) & 1023) * Q_T2 + b, J3 = (code >> 20) * Q_T3 + c;
+    const bool okc = J3 < n3;
+    const bool in00 = okc && J1 < n1 && J2 < n2, in10 = okc && J1 + 2 < n1 && J2 < n2;
+    const bool in01 = okc && J1 < n1 && J2 + 2 < n2, in11 = okc && J1 + 2 < n1 && J2 + 2 < n2;
+    const int col = (J1 * n2 + J2) * n3 + J3;  // n1 n2 n3 <= 2^24
+    // y (and v for DOT) at plane p - 4 of the step about to run, advanced by one plane per step
+    double2* yq = y + col + (int64_t)(ps0 - Q_H) * plane;
+    const double2* vqp = v + col + (int64_t)(ps0 - Q_H) * plane;
+
+    // ring of partial outputs, slot = plane mod 8; index [point][slot], points 00, 10, 01, 11
+    double2 R[4][8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) R[k][i] = make_double2(0.0, 0.0);
+
+    for (int pb = ps0 - ps0 % 8; pb < phi + Q_H; pb += 8) {
+      unroll<8>([&](auto UU) {
+        constexpr int U = decltype(UU)::value;
+        const int p = pb + U;
+        if (p < ps0 || p >= phi + Q_H) return;
+        constexpr int SQ = (U + 4) & 7;  // slot of y(p-4), then of y(p+4)
+        double2 vq[4];
+        if (DOT) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) vq[k] = make_double2(0.0, 0.0);
+          if (p - Q_H >= plo) {
+            const double2* vb = vqp;
+            if (in00) vq[0] = __ldg(vb);
+            if (in10) vq[1] = __ldg(vb + s1);
+            if (in01) vq[2] = __ldg(vb + s2);
+            if (in11) vq[3] = __ldg(vb + s1 + s2);
+          }
+        }
+        if (p < pe) {
+          if (tid == 0) issue_next();
+          f1_mbar_wait(&full[cs], (unsigned)(cu & 1));
+          const double2* st = stg + (size_t)cs * Q_STAGE;
+          // march-axis weights of plane p (uniform over the CTA)
+          const double* Wp = W + p * F1_WROW;
+          const double2 wa = *(const double2*)(Wp);
+          const double2 wc = *(const double2*)(Wp + 4);
+          const double wd = Wp[6];
+          // axis-1 weights of rows a, a+2 (uniform over the warp: broadcast loads, no registers
+          // held across the march)
+          const double* A1a = T1w + J1 * Q_T1W;
+          const double* A1b = A1a + 2 * Q_T1W;
+          const double* A2a = T2w + J2 * Q_T1W;
+          const double* A2b = A2a + 2 * Q_T1W;
+          const double* A3 = T3w + J3;
+          double2 z[4];
+          // phase A: axis-1 band + diagonal at axis-2 rows b and b + 2, into the slots of y(p)
+          {
+            const double2 wa01 = *(const double2*)(A1a), wa23 = *(const double2*)(A1a + 2);
+            const double2 wb01 = *(const double2*)(A1b), wb23 = *(const double2*)(A1b + 2);
+            const double dg = A3[4 * Q_T3N] + wa.x;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int o = oc + h * 2 * Q_RW;
+              const double2 m4 = st[o - 4 * Q_R1], m2 = st[o - 2 * Q_R1], z0 = st[o], p2 = st[o + 2 * Q_R1],
+                            p4 = st[o + 4 * Q_R1], p6 = st[o + 6 * Q_R1];
+              const double d2 = (h ? A2b[4] : A2a[4]) + dg;
+              const double da = A1a[6] + d2, db = A1b[6] + d2;
+              double2& ra = R[2 * h][U];
+              double2& rb = R[2 * h + 1][U];
+              z[2 * h] = z0;
+              z[2 * h + 1] = p2;
+              fma2(da, z0, ra);
+              fma2(wa01.x, m4, ra);
+              fma2(wa01.y, m2, ra);
+              fma2(wa23.x, p2, ra);
+              fma2(wa23.y, p4, ra);
+              fma2(db, p2, rb);
+              fma2(wb01.x, m2, rb);
+              fma2(wb01.y, z0, rb);
+              fma2(wb23.x, p4, rb);
+              fma2(wb23.y, p6, rb);
+            }
+          }
+          // phase E (needs only the centres): march-axis band terms of the centres; y(p-4) receives its last term
+          {
+            const double2 wb = *(const double2*)(Wp + 2);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              fma2(wa.y, z[k], R[k][(U + 2) & 7]);
+              fma2(wb.x, z[k], R[k][(U + 6) & 7]);
+              fma2(wc.x, z[k], R[k][SQ]);
+            }
+            if (p - Q_H >= plo) {
+              double2* yb = yq;
+              if (in00) __stcs(yb, R[0][SQ]);
+              if (in10) __stcs(yb + s1, R[1][SQ]);
+              if (in01) __stcs(yb + s2, R[2][SQ]);
+              if (in11) __stcs(yb + s1 + s2, R[3][SQ]);
+              if (DOT) {
+                cdot_acc(vq[0], R[0][SQ], dacc);
+                cdot_acc(vq[1], R[1][SQ], dacc);
+                cdot_acc(vq[2], R[2][SQ], dacc);
+                cdot_acc(vq[3], R[3][SQ], dacc);
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) R[k][SQ] = make_double2(wb.y * z[k].x, wb.y * z[k].y);  // y(p+4)
+          }
+          Q_FENCE();
+          // axis-2 taps: point b uses t = b-4, b-2, (b+2 = centre of point b+2), b+4;
+          //              point b+2 uses b-2, (b = centre of point b), b+4, b+6
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int el = h ? dlo : 0, eh = h ? dhi : 0;
+            const double2 t0 = st[o2a[0] + el], t1 = st[o2a[1] + el], t2 = st[o2a[2] + eh], t3 = st[o2a[3] + eh];
+            const double2 wa01 = *(const double2*)(A2a), wa23 = *(const double2*)(A2a + 2);
+            const double2 wb01 = *(const double2*)(A2b), wb23 = *(const double2*)(A2b + 2);
+            double2& ra = R[h][U];      // (row a or a+2, b)
+            double2& rb = R[h + 2][U];  // (row a or a+2, b+2)
+            fma2(wa01.x, t0, ra);
+            fma2(wa01.y, t1, ra);
+            fma2(wa23.x, z[h + 2], ra);
+            fma2(wa23.y, t2, ra);
+            fma2(wb01.x, t1, rb);
+            fma2(wb01.y, z[h], rb);
+            fma2(wb23.x, t2, rb);
+            fma2(wb23.y, t3, rb);
+            Q_FENCE();
+          }
+          // phase C: coupling g = G(X_1) v at rows a, a+2, scattered through T_r0(X_0) to y(p +- 1)
+          if (NMIX) {
+            const double2 ga = *(const double2*)(A1a + 4), gb = *(const double2*)(A1b + 4);
+            const double2 wcd = make_double2(wc.y, wd);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int o = oc + h * 2 * Q_RW;
+              const double2 m1 = st[o - Q_R1], p1 = st[o + Q_R1], p3 = st[o + 3 * Q_R1];
+              double2* Ra = R[2 * h];
+              double2* Rb = R[2 * h + 1];
+              double2 g = make_double2(ga.x * m1.x, ga.x * m1.y);
+              fma2(ga.y, p1, g);
+              fma2(wcd.x, g, Ra[(U + 1) & 7]);
+              fma2(wcd.y, g, Ra[(U + 7) & 7]);
+              g = make_double2(gb.x * p1.x, gb.x * p1.y);
+              fma2(gb.y, p3, g);
+              fma2(wcd.x, g, Rb[(U + 1) & 7]);
+              fma2(wcd.y, g, Rb[(U + 7) & 7]);
+            }
+            Q_FENCE();
+          }
+          // axis-3 taps (contiguous rows of A1)
+          const double w3[4] = {A3[0], A3[Q_T3N], A3[2 * Q_T3N], A3[3 * Q_T3N]};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int o = oc + (k & 1) * 2 * Q_R1 + (k >> 1) * 2 * Q_RW;
+            const double2 t0 = st[o - 4], t1 = st[o - 2], t2 = st[o + 2], t3 = st[o + 4];
+            fma2(w3[0], t0, R[k][U]);
+            fma2(w3[1], t1, R[k][U]);
+            fma2(w3[2], t2, R[k][U]);
+            fma2(w3[3], t3, R[k][U]);
+            if (k & 1) Q_FENCE();
+          }
+          __syncwarp();
+          if (lane == 0) f1_mbar_arrive(&empty[cs]);
+          if (++cs == Q_S) {
+            cs = 0;
+            ++cu;
+          }
+        } else {
+          // past the last input plane: y(p-4) only drains
+          if (p - Q_H >= plo) {
+            double2* yb = yq;
+            if (in00) __stcs(yb, R[0][SQ]);
+            if (in10) __stcs(yb + s1, R[1][SQ]);
+            if (in01) __stcs(yb + s2, R[2][SQ]);
+            if (in11) __stcs(yb + s1 + s2, R[3][SQ]);
+            if (DOT) {
+              cdot_acc(vq[0], R[0][SQ], dacc);
+              cdot_acc(vq[1], R[1][SQ], dacc);
+              cdot_acc(vq[2], R[2][SQ], dacc);
+              cdot_acc(vq[3], R[3][SQ], dacc);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) R[k][SQ] = make_double2(0.0, 0.0);
+        }
+        yq += plane;
+        if (DOT) vqp += plane;
+      });
+    }
+  }
+  if (DOT) {
+    dacc = block_sum2(dacc);
+    if (tid == 0) dotp[blockIdx.x] = dacc;
+  }
+}
+
+}  // namespace hp

@@ -208,6 +208,7 @@ __global__ void k_fg_combine(const double* __restrict__ basis, double* __restric
 
 #include "hp_fullgrid_kernels.cuh"
 #include "hp_fg1.cuh"
+#include "hp_fg4.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -242,11 +243,10 @@ static bool tma_map(CUtensorMap* m, const void* base, const int side[4], unsigne
 
 // tile order: 3x3 blocks of (i1, i2) columns, i3 fastest, so that the ~148 tiles in
 // flight form a compact block whose halos are shared through L2
-static hp_status ensure_tiles(const hp_set_s* s) {
+static hp_status make_tiles(const hp_set_s* s, int T1, int T2, int T3, int** out, int* nout) {
   std::lock_guard<std::mutex> g(s->fg_mtx);
-  if (s->fg_tiles) return HP_OK;
-  const int t1 = (s->side[1] + F1_T1 - 1) / F1_T1, t2 = (s->side[2] + F1_T2 - 1) / F1_T2,
-            t3 = (s->side[3] + F1_T3 - 1) / F1_T3;
+  if (*out) return HP_OK;
+  const int t1 = (s->side[1] + T1 - 1) / T1, t2 = (s->side[2] + T2 - 1) / T2, t3 = (s->side[3] + T3 - 1) / T3;
   int BE = 3;  // block edge in tiles (HP_FG_BLOCK overrides)
   if (const char* e = getenv("HP_FG_BLOCK")) BE = std::max(1, atoi(e));
   std::vector<int> codes;
@@ -259,9 +259,12 @@ static hp_status ensure_tiles(const hp_set_s* s) {
   int* d = nullptr;
   HP_CUDA(cudaMalloc(&d, codes.size() * sizeof(int)));
   HP_CUDA(cudaMemcpy(d, codes.data(), codes.size() * sizeof(int), cudaMemcpyHostToDevice));
-  s->fg_ntiles = (int)codes.size();
-  s->fg_tiles = d;
+  *nout = (int)codes.size();
+  *out = d;
   return HP_OK;
+}
+static hp_status ensure_tiles(const hp_set_s* s) {
+  return make_tiles(s, F1_T1, F1_T2, F1_T3, &s->fg_tiles, &s->fg_ntiles);
 }
 
 static bool fg_single_enabled() {
@@ -270,6 +273,14 @@ static bool fg_single_enabled() {
     return e && atoi(e) == 0 ? 0 : 1;
   }();
   return v == 1;
+}
+
+static int fg_quad() {  // HP_FG_QUAD=0 selects the 512-point k_fg_single instead of k_fg_quad
+  static int v = [] {
+    const char* e = getenv("HP_FG_QUAD");
+    return e && atoi(e) == 0 ? 0 : 1;
+  }();
+  return v;
 }
 
 static int fg_np() {  // points per thread of the single-pass kernel (HP_FG_NP = 1 or 2)
@@ -304,6 +315,24 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
   if (phi < 0) phi = s->side[0];
   *launched = false;
   CUtensorMap mA1, mB2;
+  if (fg_quad() && s->side[0] <= Q_MAXN && s->side[1] <= Q_MAXN) {
+    if (!tma_map(&mA1, v, s->side, 2 * Q_RW, Q_T2, Q_T1 + 2 * Q_H) || !tma_map(&mB2, v, s->side, 2 * Q_T3, Q_H, Q_T1))
+      return HP_OK;
+    hp_status rc = make_tiles(s, Q_T1, Q_T2, Q_T3, &s->fg_tiles4, &s->fg_ntiles4);
+    if (rc) return rc;
+    const int n0 = s->side[0];
+    const double* B0 = s->fg_basis + (size_t)(NMIX ? F.r0[0] : 0) * n0 * FG_W;
+    const int grid = std::min(s->fg_ntiles4, sm_count());
+    const bool use_dot = dot && dot->partial && grid <= dot->capacity;
+    auto kern = use_dot ? k_fg_quad<NMIX, true> : k_fg_quad<NMIX, false>;
+    HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
+    kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
+                                     s->side[2], s->side[3], use_dot ? dot->partial : nullptr, fg_exp(), plo, phi);
+    HP_LAUNCH_CHECK("k_fg_quad");
+    if (use_dot) dot->n = grid;
+    *launched = true;
+    return HP_OK;
+  }
   if (!tma_map(&mA1, v, s->side, 2 * F1_RW, F1_T2, F1_T1 + 2 * F1_H) ||
       !tma_map(&mB2, v, s->side, 2 * F1_T3, F1_H, F1_T1))
     return HP_OK;  // no driver entry point: the two-pass kernels run

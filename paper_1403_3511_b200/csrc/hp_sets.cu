@@ -500,6 +500,7 @@ hp_status hp_set_destroy(hp_set_t s) {
   if (s->d_off) cudaFree(s->d_off);
   if (s->fg_basis) cudaFree(s->fg_basis);
   if (s->fg_tiles) cudaFree(s->fg_tiles);
+  if (s->fg_tiles4) cudaFree(s->fg_tiles4);
   delete s;
   return HP_OK;
 }
