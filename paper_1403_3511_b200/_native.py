@@ -14,7 +14,7 @@ import threading
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "_lib" / "libhprop_b200.so"
+LIB_PATH = _HERE / "_lib" / os.environ.get("HP_LIB_VARIANT", "libhprop_b200.so")
 
 HP_OK, HP_ERR_VALUE, HP_ERR_RUNTIME, HP_ERR_CUDA, HP_ERR_NOMEM, HP_ERR_KEY = range(6)
 HP_F64, HP_C128 = 0, 1

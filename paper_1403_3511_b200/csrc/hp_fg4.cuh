@@ -17,6 +17,9 @@
 // 64 B fills + 168 B loads, against 80 + 200 for k_fg_single.
 #pragma once
 
+#ifndef Q_CONST
+#define Q_CONST 0
+#endif
 #ifndef Q_FENCES
 #define Q_FENCES 1
 #endif
@@ -31,6 +34,7 @@
 namespace hp {
 
 constexpr int Q_T1 = 8, Q_T2 = 8, Q_T3 = 16;
+constexpr int Q_MAXN = 128;  // largest side the weight tables are sized for (larger cubes: k_fg_single)
 constexpr int Q_H = FG_K;
 constexpr int Q_NT = 256;
 constexpr int Q_POINTS = Q_T1 * Q_T2 * Q_T3;
@@ -48,13 +52,62 @@ constexpr unsigned Q_STAGE_BYTES = Q_STAGE * 16u;
 constexpr int Q_S = Q_STAGES;
 constexpr size_t Q_WOFF = (size_t)Q_S * Q_STAGE_BYTES;
 constexpr int Q_T1W = 8;  // doubles per axis-1 weight row
-constexpr int Q_MAXN = 128;  // largest side the shared tables are sized for (larger cubes: k_fg_single)
-constexpr size_t Q_TOFF = Q_WOFF + (size_t)Q_MAXN * F1_WROW * sizeof(double);
-constexpr size_t Q_T2OFF = Q_TOFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
-constexpr size_t Q_T3OFF = Q_T2OFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
+constexpr size_t Q_TOFF = Q_WOFF + (Q_CONST ? 0 : (size_t)Q_MAXN * F1_WROW * sizeof(double));
+constexpr size_t Q_T2OFF = Q_TOFF + (Q_CONST ? 0 : (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double));
+constexpr size_t Q_T3OFF = Q_T2OFF + (Q_CONST ? 0 : (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double));
 constexpr int Q_T3N = Q_MAXN + 16;  // axis-3 table: [5][Q_T3N], transposed (16 lanes read 128 B)
 constexpr size_t Q_BOFF = Q_T3OFF + (size_t)5 * Q_T3N * sizeof(double);
-constexpr size_t Q_SMEM = Q_BOFF + 2 * Q_S * sizeof(uint64_t) + 8 * sizeof(int);
+constexpr int Q_TC = 64;  // tile codes cached in shared memory
+constexpr size_t Q_SMEM = Q_BOFF + 2 * Q_S * sizeof(uint64_t) + (Q_S + Q_TC) * sizeof(int);
+
+// Weight tables of the march axis (W rows) and of axes 1, 2 (T1, T2 rows), read through the
+// constant cache: every access is uniform over a warp (W: over the CTA; T1: a warp owns one
+// axis-1 row pair; T2: two rows per warp), so they cost neither registers nor shared-memory
+// wavefronts.  Filled per launch from the combined bands by k_fg_qtables + a stream-ordered copy.
+constexpr int Q_CW_W = 0;                                // [Q_MAXN][8]  march-axis rows
+constexpr int Q_CW_T1 = Q_CW_W + Q_MAXN * 8;             // [Q_MAXN + 8][8] axis-1 rows
+constexpr int Q_CW_T2 = Q_CW_T1 + (Q_MAXN + 8) * 8;      // [Q_MAXN + 8][8] axis-2 rows
+constexpr int Q_CW_N = Q_CW_T2 + (Q_MAXN + 8) * 8;
+__constant__ double q_cw[Q_CW_N];
+
+// rows: W[q]  = {P0(q,0), P0(q+2,-2), P0(q-2,2), P0(q+4,-4), P0(q-4,4), B0(q+1,-1), B0(q-1,1), 0}
+//       T1[r] = {P1(r,-4), P1(r,-2), P1(r,2), P1(r,4), G(r,-1), G(r,+1), P1(r,0), 0}
+//       T2[r] = {P2(r,-4), P2(r,-2), P2(r,2), P2(r,4), P2(r,0), 0, 0, 0}   (zeros past the cube)
+template <int NMIX>
+__device__ __forceinline__ void q_table_entry(double* out, int i, const double* P, const double* G, const double* B0,
+                                              int n0, int n1, int n2) {
+  const double* P0 = P;
+  const double* P1 = P + FG_MAXN * FG_W;
+  const double* P2 = P + 2 * FG_MAXN * FG_W;
+  const int e = i & 7;
+  double w = 0.0;
+  if (i < Q_CW_T1) {
+    const int q = i >> 3;
+    auto p0 = [&](int r, int d) { return (q < n0 && r >= 0 && r < n0) ? P0[r * FG_W + d + FG_K] : 0.0; };
+    auto b0 = [&](int r, int d) { return (NMIX && q < n0 && r >= 0 && r < n0) ? B0[r * FG_W + d + FG_K] : 0.0; };
+    const int rs[7] = {q, q + 2, q - 2, q + 4, q - 4, q + 1, q - 1};
+    const int ds[7] = {0, -2, 2, -4, 4, -1, 1};
+    if (e < 5) w = p0(rs[e], ds[e]);
+    else if (e < 7) w = b0(rs[e], ds[e]);
+  } else if (i < Q_CW_T2) {
+    const int r = (i - Q_CW_T1) >> 3;
+    const int ds[8] = {-4, -2, 2, 4, -1, 1, 0, 0};
+    if (r < n1 && e < 4) w = P1[r * FG_W + ds[e] + FG_K];
+    else if (r < n1 && e < 6) w = NMIX ? G[r * FG_W + ds[e] + FG_K] : 0.0;
+    else if (r < n1 && e == 6) w = P1[r * FG_W + FG_K];
+  } else {
+    const int r = (i - Q_CW_T2) >> 3;
+    const int ds[5] = {-4, -2, 2, 4, 0};
+    if (r < n2 && e < 5) w = P2[r * FG_W + ds[e] + FG_K];
+  }
+  out[i] = w;
+}
+template <int NMIX>
+__global__ void k_fg_qtables(double* __restrict__ out, const double* __restrict__ P, const double* __restrict__ G,
+                             const double* __restrict__ B0, int n0, int n1, int n2) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q_CW_N; i += gridDim.x * blockDim.x)
+    q_table_entry<NMIX>(out, i, P, G, B0, n0, n1, n2);
+}
 
 __device__ __forceinline__ void q_prefetch4(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
   asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(
@@ -91,6 +144,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+#if !Q_CONST
   // per-plane scatter weights (k_fg_single's row layout):
   // {P0(p,0), P0(p+2,-2), P0(p-2,2), P0(p+4,-4), P0(p-4,4), B0(p+1,-1), B0(p-1,1), 0}
   for (int q = tid; q < n0; q += Q_NT) {
@@ -131,6 +185,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
     w[4] = ok ? P2[r * FG_W + FG_K] : 0.0;
     w[5] = w[6] = w[7] = 0.0;
   }
+#endif
   // axis-3 columns, transposed: T3w[i][r] = P3(r, -4, -2, 2, 4, 0 for i = 0..4)
   for (int r = tid; r < Q_T3N; r += Q_NT) {
     const bool ok = r < n3;
@@ -145,22 +200,18 @@ __global__ void __launch_bounds__(Q_NT, 1)
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int ps0 = max(plo - Q_H, 0), pe = min(phi + Q_H, n0), nper = pe - ps0;
   const int nitems = my_tiles * nper;
-  int* ps_ = (int*)(empty + Q_S);
-  if (tid == 0) {
-    for (int i = 0; i < 8; ++i) ps_[i] = 0;
-    ps_[2] = ps0;
-  }
-  auto issue_next = [&]() {
-    int pk = ps_[0], pti = ps_[1], pp = ps_[2], ps = ps_[3], pu = ps_[4];
-    if (pk >= nitems) return;
-    if (pu > 0) f1_mbar_wait(&empty[ps], (unsigned)((pu - 1) & 1));
-    if (pp == ps0) {
-      const int code = __ldg(tiles + blockIdx.x + pti * gridDim.x);
-      ps_[5] = (code & 1023) * Q_T1;
-      ps_[6] = ((code >> 10) & 1023) * Q_T2;
-      ps_[7] = (code >> 20) * Q_T3;
-    }
-    const int T1 = ps_[5], T2 = ps_[6], T3 = ps_[7];
+  // Stage refills: the LAST warp to release a stage (smem counter per stage) refills it with the
+  // item S steps later, so no warp ever waits for the slowest one before issuing, and a fill is
+  // issued the moment its stage is free.  Item k = (tile k / nper, plane ps0 + k % nper).
+  int* cnt = (int*)(empty + Q_S);  // [Q_S] release counters
+  int* tcode = cnt + Q_S;          // this CTA's tile codes (first Q_TC)
+  for (int i = tid; i < Q_S; i += Q_NT) cnt[i] = 0;
+  for (int i = tid; i < min(my_tiles, Q_TC); i += Q_NT) tcode[i] = __ldg(tiles + blockIdx.x + i * gridDim.x);
+  __syncthreads();
+  auto issue_item = [&](int k, int ps) {
+    const int ti = k / nper, pp = ps0 + k % nper;
+    const int code = ti < Q_TC ? tcode[ti] : __ldg(tiles + blockIdx.x + ti * gridDim.x);
+    const int T1 = (code & 1023) * Q_T1, T2 = ((code >> 10) & 1023) * Q_T2, T3 = (code >> 20) * Q_T3;
     double2* dst = stg + (size_t)ps * Q_STAGE;
     uint64_t* bar = &full[ps];
     f1_mbar_expect(bar, Q_STAGE_BYTES);
@@ -168,31 +219,10 @@ __global__ void __launch_bounds__(Q_NT, 1)
     f1_tma4_hint(dst, &mA1, 2 * (T3 - Q_H), T2, T1 - Q_H, pp, bar, pol);
     f1_tma4_hint(dst + Q_OFF_LO, &mB2, 2 * T3, T2 - Q_H, T1, pp, bar, pol);
     f1_tma4_hint(dst + Q_OFF_HI, &mB2, 2 * T3, T2 + Q_T2, T1, pp, bar, pol);
-    // L2 prefetch of the same boxes PD planes ahead (HP_FG_EXP bits 8-15; 0 = off): turns the
-    // TMA fills of later planes into L2 hits
-    const int PD = (exp >> 8) & 255;
-    if (PD && pp + PD < pe) {
-      q_prefetch4(&mA1, 2 * (T3 - Q_H), T2, T1 - Q_H, pp + PD);
-      q_prefetch4(&mB2, 2 * T3, T2 - Q_H, T1, pp + PD);
-      q_prefetch4(&mB2, 2 * T3, T2 + Q_T2, T1, pp + PD);
-    }
-    ++pk;
-    if (++pp == pe) {
-      pp = ps0;
-      ++pti;
-    }
-    if (++ps == Q_S) {
-      ps = 0;
-      ++pu;
-    }
-    ps_[0] = pk;
-    ps_[1] = pti;
-    ps_[2] = pp;
-    ps_[3] = ps;
-    ps_[4] = pu;
   };
   if (tid == 0)
-    for (int k = 0; k < Q_S - 1; ++k) issue_next();
+    for (int k = 0; k < min(Q_S, nitems); ++k) issue_item(k, k);
+  int kk = 0;  // this thread's item index
 
   // centre of point (a, b) in A1; the other three points are +2 rows along axes 1 / 2
   const int oc = (a + Q_H) * Q_R1 + b * Q_RW + c + Q_H;
@@ -253,34 +283,41 @@ __global__ void __launch_bounds__(Q_NT, 1)
           }
         }
         if (p < pe) {
-          if (tid == 0) issue_next();
           f1_mbar_wait(&full[cs], (unsigned)(cu & 1));
           const double2* st = stg + (size_t)cs * Q_STAGE;
           // march-axis weights of plane p (uniform over the CTA)
-          const double* Wp = W + p * F1_WROW;
-          const double2 wa = *(const double2*)(Wp);
-          const double2 wc = *(const double2*)(Wp + 4);
-          const double wd = Wp[6];
+#if Q_CONST
+#define QW(i) q_cw[Q_CW_W + p * 8 + (i)]
+#define QT1A(i) q_cw[Q_CW_T1 + J1 * 8 + (i)]
+#define QT1B(i) q_cw[Q_CW_T1 + J1 * 8 + 16 + (i)]
+#define QT2A(i) q_cw[Q_CW_T2 + J2 * 8 + (i)]
+#define QT2B(i) q_cw[Q_CW_T2 + J2 * 8 + 16 + (i)]
+#else
+#define QW(i) W[p * F1_WROW + (i)]
+#define QT1A(i) T1w[J1 * Q_T1W + (i)]
+#define QT1B(i) T1w[J1 * Q_T1W + 2 * Q_T1W + (i)]
+#define QT2A(i) T2w[J2 * Q_T1W + (i)]
+#define QT2B(i) T2w[J2 * Q_T1W + 2 * Q_T1W + (i)]
+#endif
+          const double2 wa = make_double2(QW(0), QW(1));
+          const double2 wc = make_double2(QW(4), QW(5));
+          const double wd = QW(6);
           // axis-1 weights of rows a, a+2 (uniform over the warp: broadcast loads, no registers
           // held across the march)
-          const double* A1a = T1w + J1 * Q_T1W;
-          const double* A1b = A1a + 2 * Q_T1W;
-          const double* A2a = T2w + J2 * Q_T1W;
-          const double* A2b = A2a + 2 * Q_T1W;
           const double* A3 = T3w + J3;
           double2 z[4];
           // phase A: axis-1 band + diagonal at axis-2 rows b and b + 2, into the slots of y(p)
           {
-            const double2 wa01 = *(const double2*)(A1a), wa23 = *(const double2*)(A1a + 2);
-            const double2 wb01 = *(const double2*)(A1b), wb23 = *(const double2*)(A1b + 2);
+            const double2 wa01 = make_double2(QT1A(0), QT1A(1)), wa23 = make_double2(QT1A(2), QT1A(3));
+            const double2 wb01 = make_double2(QT1B(0), QT1B(1)), wb23 = make_double2(QT1B(2), QT1B(3));
             const double dg = A3[4 * Q_T3N] + wa.x;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int o = oc + h * 2 * Q_RW;
               const double2 m4 = st[o - 4 * Q_R1], m2 = st[o - 2 * Q_R1], z0 = st[o], p2 = st[o + 2 * Q_R1],
                             p4 = st[o + 4 * Q_R1], p6 = st[o + 6 * Q_R1];
-              const double d2 = (h ? A2b[4] : A2a[4]) + dg;
-              const double da = A1a[6] + d2, db = A1b[6] + d2;
+              const double d2 = (h ? QT2B(4) : QT2A(4)) + dg;
+              const double da = QT1A(6) + d2, db = QT1B(6) + d2;
               double2& ra = R[2 * h][U];
               double2& rb = R[2 * h + 1][U];
               z[2 * h] = z0;
@@ -299,7 +336,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
           }
           // phase E (needs only the centres): march-axis band terms of the centres; y(p-4) receives its last term
           {
-            const double2 wb = *(const double2*)(Wp + 2);
+            const double2 wb = make_double2(QW(2), QW(3));
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               fma2(wa.y, z[k], R[k][(U + 2) & 7]);
@@ -329,8 +366,8 @@ __global__ void __launch_bounds__(Q_NT, 1)
           for (int h = 0; h < 2; ++h) {
             const int el = h ? dlo : 0, eh = h ? dhi : 0;
             const double2 t0 = st[o2a[0] + el], t1 = st[o2a[1] + el], t2 = st[o2a[2] + eh], t3 = st[o2a[3] + eh];
-            const double2 wa01 = *(const double2*)(A2a), wa23 = *(const double2*)(A2a + 2);
-            const double2 wb01 = *(const double2*)(A2b), wb23 = *(const double2*)(A2b + 2);
+            const double2 wa01 = make_double2(QT2A(0), QT2A(1)), wa23 = make_double2(QT2A(2), QT2A(3));
+            const double2 wb01 = make_double2(QT2B(0), QT2B(1)), wb23 = make_double2(QT2B(2), QT2B(3));
             double2& ra = R[h][U];      // (row a or a+2, b)
             double2& rb = R[h + 2][U];  // (row a or a+2, b+2)
             fma2(wa01.x, t0, ra);
@@ -345,7 +382,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
           }
           // phase C: coupling g = G(X_1) v at rows a, a+2, scattered through T_r0(X_0) to y(p +- 1)
           if (NMIX) {
-            const double2 ga = *(const double2*)(A1a + 4), gb = *(const double2*)(A1b + 4);
+            const double2 ga = make_double2(QT1A(4), QT1A(5)), gb = make_double2(QT1B(4), QT1B(5));
             const double2 wcd = make_double2(wc.y, wd);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -377,7 +414,15 @@ __global__ void __launch_bounds__(Q_NT, 1)
             if (k & 1) Q_FENCE();
           }
           __syncwarp();
-          if (lane == 0) f1_mbar_arrive(&empty[cs]);
+          if (lane == 0) {
+            f1_mbar_arrive(&empty[cs]);
+            if (atomicAdd(&cnt[cs], 1) == Q_NT / 32 - 1) {
+              cnt[cs] = 0;
+              f1_mbar_wait(&empty[cs], (unsigned)(cu & 1));  // all releases landed (acquire)
+              if (kk + Q_S < nitems) issue_item(kk + Q_S, cs);
+            }
+          }
+          ++kk;
           if (++cs == Q_S) {
             cs = 0;
             ++cu;

@@ -326,9 +326,32 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
     const bool use_dot = dot && dot->partial && grid <= dot->capacity;
     auto kern = use_dot ? k_fg_quad<NMIX, true> : k_fg_quad<NMIX, false>;
     HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
+#if Q_CONST
+    // the weight tables live in one per-device constant buffer: launches that use it are
+    // serialised across streams (each waits for the previous user's kernel before overwriting)
+    static std::mutex q_mtx;
+    static cudaEvent_t q_ev[64] = {};
+    static double* q_stage[64] = {};
+    std::lock_guard<std::mutex> lk(q_mtx);
+    int dev = 0;
+    HP_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return HP_ERR_CUDA;
+    if (!q_ev[dev]) {
+      HP_CUDA(cudaEventCreateWithFlags(&q_ev[dev], cudaEventDisableTiming));
+      HP_CUDA(cudaMalloc(&q_stage[dev], Q_CW_N * sizeof(double)));
+    } else {
+      HP_CUDA(cudaStreamWaitEvent(st, q_ev[dev], 0));
+    }
+    k_fg_qtables<NMIX><<<(Q_CW_N + 255) / 256, 256, 0, st>>>(q_stage[dev], P, G, B0, n0, s->side[1], s->side[2]);
+    HP_LAUNCH_CHECK("k_fg_qtables");
+    HP_CUDA(cudaMemcpyToSymbolAsync(q_cw, q_stage[dev], Q_CW_N * sizeof(double), 0, cudaMemcpyDeviceToDevice, st));
+#endif
     kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
                                      s->side[2], s->side[3], use_dot ? dot->partial : nullptr, fg_exp(), plo, phi);
     HP_LAUNCH_CHECK("k_fg_quad");
+#if Q_CONST
+    HP_CUDA(cudaEventRecord(q_ev[dev], st));
+#endif
     if (use_dot) dot->n = grid;
     *launched = true;
     return HP_OK;

@@ -1,3 +1,7 @@
-HP_FG_QUAD=0 timeout 120 python tools/time_matvec.py cfg4 20
-for pd in 0 2 4 8; do echo pd=$pd; HP_FG_EXP=$((pd*256)) timeout 120 python tools/time_matvec.py cfg4 20; done
-timeout 900 python -m pytest tests/test_gpu_matvec.py -x -q -k "fused or cfg4 or slab or stream or random" > gpurun_out/pytest_matvec.log 2>&1; echo rc=$?; tail -2 gpurun_out/pytest_matvec.log
+for v in libhprop_b200.so libhprop_b200_smemw.so libhprop_b200.so libhprop_b200_smemw.so; do
+echo $v; HP_LIB_VARIANT=$v timeout 120 python tools/time_matvec.py cfg4 20
+done
+for v in libhprop_b200.so libhprop_b200_smemw.so; do
+HP_LIB_VARIANT=$v timeout 300 python tools/bench_propagate.py cfg4 --steps 5 --cpu-steps 0 2>&1 | tail -1
+done
+HP_FG_QUAD=0 timeout 300 python tools/bench_propagate.py cfg4 --steps 5 --cpu-steps 0 2>&1 | tail -1
