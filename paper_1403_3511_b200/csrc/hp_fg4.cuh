@@ -20,6 +20,9 @@
 #ifndef Q_CONST
 #define Q_CONST 0
 #endif
+#ifndef Q_WREG
+#define Q_WREG 0
+#endif
 #ifndef Q_FENCES
 #define Q_FENCES 1
 #endif
@@ -253,6 +256,29 @@ __global__ void __launch_bounds__(Q_NT, 1)
     const bool in00 = okc && J1 < n1 && J2 < n2, in10 = okc && J1 + 2 < n1 && J2 < n2;
     const bool in01 = okc && J1 < n1 && J2 + 2 < n2, in11 = okc && J1 + 2 < n1 && J2 + 2 < n2;
     const int col = (J1 * n2 + J2) * n3 + J3;  // n1 n2 n3 <= 2^24
+    // Q_WREG: band weights held in registers for the whole tile march instead of per-plane
+    // shared loads (bit 0: axis 1, bit 1: axis 2, bit 2: axis 3)
+#if Q_WREG & 1
+    double r1a[7], r1b[7];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      r1a[i] = T1w[J1 * Q_T1W + i];
+      r1b[i] = T1w[J1 * Q_T1W + 2 * Q_T1W + i];
+    }
+#endif
+#if Q_WREG & 2
+    double r2a[5], r2b[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      r2a[i] = T2w[J2 * Q_T1W + i];
+      r2b[i] = T2w[J2 * Q_T1W + 2 * Q_T1W + i];
+    }
+#endif
+#if Q_WREG & 4
+    double r3[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) r3[i] = T3w[i * Q_T3N + J3];
+#endif
     // y (and v for DOT) at plane p - 4 of the step about to run, advanced by one plane per step
     double2* yq = y + col + (int64_t)(ps0 - Q_H) * plane;
     const double2* vqp = v + col + (int64_t)(ps0 - Q_H) * plane;
@@ -286,6 +312,11 @@ __global__ void __launch_bounds__(Q_NT, 1)
           f1_mbar_wait(&full[cs], (unsigned)(cu & 1));
           const double2* st = stg + (size_t)cs * Q_STAGE;
           // march-axis weights of plane p (uniform over the CTA)
+#if Q_WREG & 4
+#define Q3(i) r3[i]
+#else
+#define Q3(i) A3[(i) * Q_T3N]
+#endif
 #if Q_CONST
 #define QW(i) q_cw[Q_CW_W + p * 8 + (i)]
 #define QT1A(i) q_cw[Q_CW_T1 + J1 * 8 + (i)]
@@ -294,10 +325,20 @@ __global__ void __launch_bounds__(Q_NT, 1)
 #define QT2B(i) q_cw[Q_CW_T2 + J2 * 8 + 16 + (i)]
 #else
 #define QW(i) W[p * F1_WROW + (i)]
+#if Q_WREG & 1
+#define QT1A(i) r1a[i]
+#define QT1B(i) r1b[i]
+#else
 #define QT1A(i) T1w[J1 * Q_T1W + (i)]
 #define QT1B(i) T1w[J1 * Q_T1W + 2 * Q_T1W + (i)]
+#endif
+#if Q_WREG & 2
+#define QT2A(i) r2a[i]
+#define QT2B(i) r2b[i]
+#else
 #define QT2A(i) T2w[J2 * Q_T1W + (i)]
 #define QT2B(i) T2w[J2 * Q_T1W + 2 * Q_T1W + (i)]
+#endif
 #endif
           const double2 wa = make_double2(QW(0), QW(1));
           const double2 wc = make_double2(QW(4), QW(5));
@@ -310,7 +351,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
           {
             const double2 wa01 = make_double2(QT1A(0), QT1A(1)), wa23 = make_double2(QT1A(2), QT1A(3));
             const double2 wb01 = make_double2(QT1B(0), QT1B(1)), wb23 = make_double2(QT1B(2), QT1B(3));
-            const double dg = A3[4 * Q_T3N] + wa.x;
+            const double dg = Q3(4) + wa.x;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int o = oc + h * 2 * Q_RW;
@@ -402,7 +443,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
             Q_FENCE();
           }
           // axis-3 taps (contiguous rows of A1)
-          const double w3[4] = {A3[0], A3[Q_T3N], A3[2 * Q_T3N], A3[3 * Q_T3N]};
+          const double w3[4] = {Q3(0), Q3(1), Q3(2), Q3(3)};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int o = oc + (k & 1) * 2 * Q_R1 + (k >> 1) * 2 * Q_RW;
