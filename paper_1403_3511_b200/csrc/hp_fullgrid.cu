@@ -209,6 +209,7 @@ __global__ void k_fg_combine(const double* __restrict__ basis, double* __restric
 #include "hp_fullgrid_kernels.cuh"
 #include "hp_fg1.cuh"
 #include "hp_fg4.cuh"
+#include "hp_fg4ri.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -283,6 +284,14 @@ static int fg_quad() {  // HP_FG_QUAD=0 selects the 512-point k_fg_single instea
   return v;
 }
 
+static bool fg_ri() {  // HP_FG_RI=1: split-component quad kernel (k_fg_quad_ri)
+  static int v = [] {
+    const char* e = getenv("HP_FG_RI");
+    return e && atoi(e) == 1 ? 1 : 0;
+  }();
+  return v == 1;
+}
+
 static int fg_np() {  // points per thread of the single-pass kernel (HP_FG_NP = 1 or 2)
   static int v = [] {
     const char* e = getenv("HP_FG_NP");
@@ -326,32 +335,44 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
     const bool use_dot = dot && dot->partial && grid <= dot->capacity;
     auto kern = use_dot ? k_fg_quad<NMIX, true> : k_fg_quad<NMIX, false>;
     HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
-#if Q_CONST
-    // the weight tables live in one per-device constant buffer: launches that use it are
-    // serialised across streams (each waits for the previous user's kernel before overwriting)
+    // the weight tables of the constant-bank variants live in one per-device constant buffer:
+    // launches that use it are serialised across streams (each waits for the previous user's
+    // kernel before overwriting)
     static std::mutex q_mtx;
     static cudaEvent_t q_ev[64] = {};
     static double* q_stage[64] = {};
-    std::lock_guard<std::mutex> lk(q_mtx);
+    std::unique_lock<std::mutex> lk(q_mtx, std::defer_lock);
     int dev = 0;
-    HP_CUDA(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= 64) return HP_ERR_CUDA;
-    if (!q_ev[dev]) {
-      HP_CUDA(cudaEventCreateWithFlags(&q_ev[dev], cudaEventDisableTiming));
-      HP_CUDA(cudaMalloc(&q_stage[dev], Q_CW_N * sizeof(double)));
-    } else {
-      HP_CUDA(cudaStreamWaitEvent(st, q_ev[dev], 0));
+    const bool ri = fg_ri();
+    if (Q_CONST || ri) {
+      lk.lock();
+      HP_CUDA(cudaGetDevice(&dev));
+      if (dev < 0 || dev >= 64) return HP_ERR_CUDA;
+      if (!q_ev[dev]) {
+        HP_CUDA(cudaEventCreateWithFlags(&q_ev[dev], cudaEventDisableTiming));
+        HP_CUDA(cudaMalloc(&q_stage[dev], Q_CW_N * sizeof(double)));
+      } else {
+        HP_CUDA(cudaStreamWaitEvent(st, q_ev[dev], 0));
+      }
+      k_fg_qtables<NMIX><<<(Q_CW_N + 255) / 256, 256, 0, st>>>(q_stage[dev], P, G, B0, n0, s->side[1], s->side[2]);
+      HP_LAUNCH_CHECK("k_fg_qtables");
+      HP_CUDA(cudaMemcpyToSymbolAsync(q_cw, q_stage[dev], Q_CW_N * sizeof(double), 0, cudaMemcpyDeviceToDevice, st));
     }
-    k_fg_qtables<NMIX><<<(Q_CW_N + 255) / 256, 256, 0, st>>>(q_stage[dev], P, G, B0, n0, s->side[1], s->side[2]);
-    HP_LAUNCH_CHECK("k_fg_qtables");
-    HP_CUDA(cudaMemcpyToSymbolAsync(q_cw, q_stage[dev], Q_CW_N * sizeof(double), 0, cudaMemcpyDeviceToDevice, st));
-#endif
+    if (ri) {
+      auto kr = use_dot ? k_fg_quad_ri<NMIX, true> : k_fg_quad_ri<NMIX, false>;
+      HP_CUDA(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM));
+      kr<<<grid, QR_NT, QR_SMEM, st>>>(mA1, mB2, v, y, P, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1], s->side[2],
+                                        s->side[3], use_dot ? dot->partial : nullptr, plo, phi);
+      HP_LAUNCH_CHECK("k_fg_quad_ri");
+      HP_CUDA(cudaEventRecord(q_ev[dev], st));
+      if (use_dot) dot->n = grid;
+      *launched = true;
+      return HP_OK;
+    }
     kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
                                      s->side[2], s->side[3], use_dot ? dot->partial : nullptr, fg_exp(), plo, phi);
     HP_LAUNCH_CHECK("k_fg_quad");
-#if Q_CONST
-    HP_CUDA(cudaEventRecord(q_ev[dev], st));
-#endif
+    if (Q_CONST) HP_CUDA(cudaEventRecord(q_ev[dev], st));
     if (use_dot) dot->n = grid;
     *launched = true;
     return HP_OK;
