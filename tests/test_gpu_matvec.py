@@ -510,3 +510,47 @@ def test_streamed_host_matvec_batch_and_flags(hp):
     assert np.array_equal(yh1.numpy(), appl.apply_polynomial(ap, v, ref_order=True))
     with pytest.raises(ValueError):
         appl.apply_host_into(ap, xh1.cuda(), yh1)
+
+
+_KERNEL_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1403_3511_b200 as hp
+from oracle import hprop_oracle as O
+from paper_1403_3511_b200 import workloads as W
+worst = 0.0
+for bound in (5, 11, 20):
+    w = W.CONFIGS["cfg4"].scaled(bound, "cfg4x")
+    ap = w.approx(0.3)
+    c = W.coefficients(w)
+    oa = O.applier_for_full(w.dim, w.bound)
+    appl = hp.get_applier(hp.build_full(w.dim, w.bound))
+    for got, want in ((appl.apply_polynomial(ap, c), oa.polynomial(ap.degrees, ap.coeffs, 16.0, c)),
+                      (appl.apply_hamiltonian(ap, c), oa.hamiltonian(ap.degrees, ap.coeffs, 16.0, c))):
+        worst = max(worst, float(np.linalg.norm(got - want) / np.linalg.norm(want)))
+    side = w.bound + 1
+    plane = side ** 3
+    lo, hi = side // 3, side
+    x = c[lo * plane:hi * plane]
+    got = hp.get_applier(hp.build_slab(w.dim, w.bound, lo, hi)).apply_hamiltonian(ap, x)
+    want = O.applier_for_slab(w.dim, w.bound, lo, hi).hamiltonian(ap.degrees, ap.coeffs, 16.0, x)
+    worst = max(worst, float(np.linalg.norm(got - want) / np.linalg.norm(want)))
+print(worst)
+"""
+
+
+@pytest.mark.parametrize("env", [{"HP_FG_QUAD": "0"}, {"HP_FG_RI": "1"}], ids=["k_fg_single", "k_fg_quad_ri"])
+def test_alternate_single_pass_kernels(env):
+    """The non-default single-pass kernels (selected once per process by environment, so run in a
+    subprocess): k_fg_single (cubes with a side > 128) and the split-component k_fg_quad_ri, on
+    cubes and a j1-slab, against the oracle."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, "-c", _KERNEL_SCRIPT, str(root)], env={**os.environ, **env},
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) < TOL
