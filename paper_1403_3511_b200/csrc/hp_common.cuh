@@ -162,6 +162,10 @@ struct hp_set_s {
   // the same for the quad kernel's 8 x 8 x 16 tiles (hp_fg4.cuh)
   mutable int* fg_tiles4 = nullptr;
   mutable int fg_ntiles4 = 0;
+  // tabled sets: per-axis line order (ordinals grouped by axis line, hp_level.cu), built on
+  // first use by the level kernels of outer axes
+  mutable std::mutex perm_mtx;
+  mutable int32_t* d_perm[HP_MAXDIM] = {nullptr};
 
   hp::AxBox box(int a) const {
     hp::AxBox v;

@@ -29,6 +29,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "hp_common.cuh"
 #include "hp_program.h"
 
@@ -324,10 +326,15 @@ template <int K, int TGN, class AX, class AXS>
 __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, AXS axs, int dim, LvLevel lv,
                                                double inv_L, double two_L, const double2* __restrict__ v,
                                                double2* __restrict__ slots, double2* __restrict__ y, int first,
-                                               int osc, double2* __restrict__ dotp) {
+                                               int osc, double2* __restrict__ dotp,
+                                               const int32_t* __restrict__ perm) {
   constexpr int S = 2 * K + 1;
   double2 dacc = make_double2(0.0, 0.0);
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    // perm (outer axes of tabled sets): line-blocked order (line_order below), so the +-K
+    // windows of neighbouring warps overlap in L1/L2 (ordinal order puts the window positions
+    // one sub-block apart, far beyond L2 reuse)
+    const int64_t o = perm ? (int64_t)__ldg(perm + t) : t;
     // the axis line through o: seg[K + d] = ordinal of j + d e_a, or -1
     int64_t seg[S];
     int jo;
@@ -440,34 +447,147 @@ struct LvAllTab {
 template <int K>
 static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, const double2* v, double2* slots,
                               double2* y, int64_t batch, int first, int osc, double2* dotp, int grid,
-                              cudaStream_t st) {
+                              cudaStream_t st, const int32_t* perm) {
   const int64_t n = s->n;
   if (s->boxed) {
     LvAllBox axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->box(a);
     if (lv.ntg <= 1)
       k_level<K, 1, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv, 1.0 / L,
-                                                          2.0 / L, v, slots, y, first, osc, dotp);
+                                                          2.0 / L, v, slots, y, first, osc, dotp, perm);
     else if (lv.ntg <= 4)
       k_level<K, 4, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv, 1.0 / L,
-                                                          2.0 / L, v, slots, y, first, osc, dotp);
+                                                          2.0 / L, v, slots, y, first, osc, dotp, perm);
     else
       k_level<K, LV_MAXTG, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv,
-                                                                 1.0 / L, 2.0 / L, v, slots, y, first, osc, dotp);
+                                                                 1.0 / L, 2.0 / L, v, slots, y, first, osc, dotp, perm);
   } else {
     LvAllTab axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
     if (lv.ntg <= 1)
       k_level<K, 1, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv, 1.0 / L,
-                                                          2.0 / L, v, slots, y, first, osc, dotp);
+                                                          2.0 / L, v, slots, y, first, osc, dotp, perm);
     else if (lv.ntg <= 4)
       k_level<K, 4, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv, 1.0 / L,
-                                                          2.0 / L, v, slots, y, first, osc, dotp);
+                                                          2.0 / L, v, slots, y, first, osc, dotp, perm);
     else
       k_level<K, LV_MAXTG, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv,
-                                                                 1.0 / L, 2.0 / L, v, slots, y, first, osc, dotp);
+                                                                 1.0 / L, 2.0 / L, v, slots, y, first, osc, dotp, perm);
   }
   HP_LAUNCH_CHECK("k_level");
+  return HP_OK;
+}
+
+// ---------------------------------------------------------------- line order of an axis
+
+// Line-blocked order: the heads (points without a -e_a neighbour) are taken in blocks of 32
+// consecutive heads; a block emits row k = the k-th points of its lines for k = 0, 1, ...  A row
+// is (nearly) contiguous in storage, so a warp's loads stay coalesced, and the rows k +- d that
+// the +-K windows read are processed by the neighbouring warps: each input element is fetched
+// from HBM about once instead of once per window position.
+// Pass 1: per block of 32 heads, the number of points of its lines (one warp per block).
+__global__ void k_line_count(int64_t nheads, const int32_t* __restrict__ heads, const int32_t* __restrict__ up,
+                             int32_t* __restrict__ bcount) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t w = w0; w * 32 < nheads; w += nw) {
+    const int64_t i = w * 32 + lane;
+    int L = 0;
+    if (i < nheads)
+      for (int64_t q = __ldg(heads + i); q >= 0; q = __ldg(up + q)) ++L;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_down_sync(0xffffffffu, L, o);
+    if (lane == 0) bcount[w] = L;
+  }
+}
+// Pass 2: each warp writes its block's rows at the block offset
+__global__ void k_line_fill(int64_t nheads, const int32_t* __restrict__ heads, const int32_t* __restrict__ up,
+                            const int32_t* __restrict__ boff, int32_t* __restrict__ perm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  for (int64_t w = w0; w * 32 < nheads; w += nw) {
+    const int64_t i = w * 32 + lane;
+    int64_t q = i < nheads ? (int64_t)__ldg(heads + i) : -1;
+    int32_t pos = __ldg(boff + w);
+    for (;;) {
+      const unsigned live = __ballot_sync(0xffffffffu, q >= 0);
+      if (!live) break;
+      if (q >= 0) {
+        perm[pos + __popc(live & ((1u << lane) - 1))] = (int32_t)q;
+        q = __ldg(up + q);
+      }
+      pos += __popc(live);
+    }
+  }
+}
+__global__ void k_line_heads_flag(int64_t n, const int32_t* __restrict__ down, int32_t* __restrict__ flag) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
+    flag[o] = __ldg(down + o) < 0 ? 1 : 0;
+}
+__global__ void k_line_heads_list(int64_t n, const int32_t* __restrict__ down, const int32_t* __restrict__ pos,
+                                  int32_t* __restrict__ heads) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x)
+    if (__ldg(down + o) < 0) heads[__ldg(pos + o)] = (int32_t)o;
+}
+
+// axes whose level kernels run in line order (HP_LEVEL_PERM: bit a = axis a).  Default: axis 1
+// of sets with N >= 4.  Measured (ms per matvec, ordinal order -> line order of the axes in the
+// mask): cfg3 7.49 -> {1} 7.27, {0,1} 7.39, {0,1,2} 7.53, {0} 7.57; cfg5 (32 vectors) 940 ->
+// {1} 835, {0,1} 831, {0,1,2} 830, {0} 936.  Axis 0 gains nothing (its level has one input and
+// its lines are the longest); axis 1 carries the widest levels of both plans.
+static unsigned perm_axes(int dim) {
+  static int env = [] {
+    const char* e = getenv("HP_LEVEL_PERM");
+    return e ? atoi(e) : -1;
+  }();
+  if (env >= 0) return (unsigned)env;
+  return dim >= 4 ? 2u : 0u;
+}
+
+// perm: the line-blocked order of the ordinals (a permutation of 0..n-1: every ordinal lies on
+// exactly one axis line, which has exactly one head)
+static hp_status line_order(const hp_set_s* s, int a, cudaStream_t st, const int32_t** out) {
+  *out = nullptr;
+  if (s->boxed || !(perm_axes(s->dim) >> a & 1) || s->n < 2 || s->n > INT32_MAX) return HP_OK;
+  std::lock_guard<std::mutex> g(s->perm_mtx);
+  if (!s->d_perm[a]) {
+    const int64_t n = s->n;
+    // heads in ordinal order: flag, exclusive scan, compact
+    int32_t *flag = nullptr, *pos = nullptr, *heads = nullptr, *perm = nullptr;
+    HP_CUDA(cudaMallocAsync(&flag, (n + 1) * sizeof(int32_t), st));
+    HP_CUDA(cudaMallocAsync(&pos, (n + 1) * sizeof(int32_t), st));
+    void* tmp = nullptr;
+    size_t tb = 0;
+    HP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, (const int32_t*)nullptr, (int32_t*)nullptr, (int)n + 1, st));
+    HP_CUDA(cudaMallocAsync(&tmp, tb, st));
+    const int grid = grid_for(n, 256);
+    HP_CUDA(cudaMemsetAsync(flag + n, 0, sizeof(int32_t), st));
+    k_line_heads_flag<<<grid, 256, 0, st>>>(n, s->d_down[a], flag);
+    HP_LAUNCH_CHECK("k_line_heads_flag");
+    HP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, pos, (int)n + 1, st));
+    int32_t nheads = 0;
+    HP_CUDA(cudaMemcpyAsync(&nheads, pos + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HP_CUDA(cudaStreamSynchronize(st));
+    HP_CUDA(cudaMallocAsync(&heads, std::max<int64_t>(nheads, 1) * sizeof(int32_t), st));
+    k_line_heads_list<<<grid, 256, 0, st>>>(n, s->d_down[a], pos, heads);
+    HP_LAUNCH_CHECK("k_line_heads_list");
+    // per-block counts -> offsets (reusing flag / pos)
+    const int64_t nb = (nheads + 31) / 32;
+    const int wgrid = grid_for(nb * 32, 256);
+    HP_CUDA(cudaMemsetAsync(flag + nb, 0, sizeof(int32_t), st));
+    k_line_count<<<wgrid, 256, 0, st>>>(nheads, heads, s->d_up[a], flag);
+    HP_LAUNCH_CHECK("k_line_count");
+    HP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, pos, (int)nb + 1, st));
+    HP_CUDA(cudaMalloc(&perm, n * sizeof(int32_t)));
+    k_line_fill<<<wgrid, 256, 0, st>>>(nheads, heads, s->d_up[a], pos, perm);
+    HP_LAUNCH_CHECK("k_line_fill");
+    HP_CUDA(cudaFreeAsync(flag, st));
+    HP_CUDA(cudaFreeAsync(pos, st));
+    HP_CUDA(cudaFreeAsync(heads, st));
+    HP_CUDA(cudaFreeAsync(tmp, st));
+    s->d_perm[a] = perm;
+  }
+  *out = s->d_perm[a];
   return HP_OK;
 }
 
@@ -518,14 +638,16 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
       const bool last = li == last_y;
       const int first = li == first_y ? 1 : 0;
       double2* dotp = (last && dot && dot->partial && batch == 1 && grid <= dot->capacity) ? dot->partial : nullptr;
-      hp_status rc;
+      const int32_t* perm = nullptr;
+      hp_status rc = line_order(s, lv.axis, st, &perm);
+      if (rc) return rc;
       const int oscf = last && osc ? 1 : 0;
       switch (lv.K) {
-        case 0: rc = launch_level<0>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
-        case 1: rc = launch_level<1>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
-        case 2: rc = launch_level<2>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
-        case 3: rc = launch_level<3>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
-        default: rc = launch_level<4>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st); break;
+        case 0: rc = launch_level<0>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
+        case 1: rc = launch_level<1>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
+        case 2: rc = launch_level<2>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
+        case 3: rc = launch_level<3>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
+        default: rc = launch_level<4>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
       }
       if (rc) return rc;
       if (dotp) dot->n = grid;
