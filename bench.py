@@ -387,8 +387,10 @@ def gpu_arm(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
                "d2h_bytes_per_step": int(yh.numel() * yh.element_size()), "ms_per_step": round(ems, 3),
                "steps": e_steps,
-               "path": ("pinned host -> HBM -> pinned host inside hp_apply_polynomial_streamed (C ABI; "
-                        "j1-plane chunks, copies overlapped with the kernels)" if sharding is None else
+               "path": ("pinned host -> HBM -> pinned host inside hp_apply_polynomial_streamed (C ABI; " +
+                        ("j1-plane chunks, copies overlapped with the kernels)" if w.kind == "full" else
+                         "groups of batch vectors, copies overlapped with the kernels)" if batch > 1 else
+                         "whole-vector copies around the matvec)") if sharding is None else
                         "pinned host -> HBM, hp_apply_polynomial (C ABI) + halo exchange, HBM -> pinned host")}
 
     cpu = None

@@ -672,12 +672,46 @@ hp_status hp_apply_polynomial_streamed(hp_set_t s, const int32_t* degrees, const
                                  ws_bytes, st, &done);
     if (rc || done) return rc;
   }
-  // other sets / term structures: whole-vector copies around the device matvec
-  HP_CUDA(cudaMemcpyAsync(in_dev, in_host, bytes, cudaMemcpyHostToDevice, st));
-  rc = hp_apply_polynomial(s, degrees, coeffs, nterms, halfwidth, dtype, in_dev, out_dev, batch, flags, nullptr, ws,
-                           ws_bytes, stream);
-  if (rc) return rc;
-  HP_CUDA(cudaMemcpyAsync(out_host, out_dev, bytes, cudaMemcpyDeviceToHost, st));
+  // other sets / term structures: the batch streams through in groups of vectors (>= 32 MB
+  // each): group k+1 is copied in and group k-1 out while group k is computed
+  const size_t vbytes = bytes / batch;
+  const int64_t g = std::min<int64_t>(batch, std::max<int64_t>(1, (int64_t)(((size_t)32 << 20) / vbytes)));
+  const int64_t ng = (batch + g - 1) / g;
+  if (ng == 1) {
+    HP_CUDA(cudaMemcpyAsync(in_dev, in_host, bytes, cudaMemcpyHostToDevice, st));
+    rc = hp_apply_polynomial(s, degrees, coeffs, nterms, halfwidth, dtype, in_dev, out_dev, batch, flags, nullptr,
+                             ws, ws_bytes, stream);
+    if (rc) return rc;
+    HP_CUDA(cudaMemcpyAsync(out_host, out_dev, bytes, cudaMemcpyDeviceToHost, st));
+    return HP_OK;
+  }
+  cudaStream_t sin, sout;
+  if ((rc = copy_streams(&sin, &sout))) return rc;
+  std::vector<cudaEvent_t> ev(2 * ng + 2);
+  for (auto& e : ev) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  HP_CUDA(cudaEventRecord(ev[2 * ng], st));  // after the caller's prior work
+  HP_CUDA(cudaStreamWaitEvent(sin, ev[2 * ng], 0));
+  HP_CUDA(cudaStreamWaitEvent(sout, ev[2 * ng], 0));
+  for (int64_t k = 0; k < ng; ++k) {
+    const int64_t b0 = k * g, nb = std::min(g, batch - b0);
+    HP_CUDA(cudaMemcpyAsync((char*)in_dev + b0 * vbytes, (const char*)in_host + b0 * vbytes, nb * vbytes,
+                            cudaMemcpyHostToDevice, sin));
+    HP_CUDA(cudaEventRecord(ev[k], sin));
+  }
+  for (int64_t k = 0; k < ng; ++k) {
+    const int64_t b0 = k * g, nb = std::min(g, batch - b0);
+    HP_CUDA(cudaStreamWaitEvent(st, ev[k], 0));
+    rc = hp_apply_polynomial(s, degrees, coeffs, nterms, halfwidth, dtype, (const char*)in_dev + b0 * vbytes,
+                             (char*)out_dev + b0 * vbytes, nb, flags, nullptr, ws, ws_bytes, stream);
+    if (rc) return rc;
+    HP_CUDA(cudaEventRecord(ev[ng + k], st));
+    HP_CUDA(cudaStreamWaitEvent(sout, ev[ng + k], 0));
+    HP_CUDA(cudaMemcpyAsync((char*)out_host + b0 * vbytes, (const char*)out_dev + b0 * vbytes, nb * vbytes,
+                            cudaMemcpyDeviceToHost, sout));
+  }
+  HP_CUDA(cudaEventRecord(ev[2 * ng + 1], sout));
+  HP_CUDA(cudaStreamWaitEvent(st, ev[2 * ng + 1], 0));
+  for (auto& e : ev) cudaEventDestroy(e);
   return HP_OK;
 }
 

@@ -578,7 +578,7 @@ hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& term
 // ---------------------------------------------------------------- streamed (host-resident vectors)
 
 // copy streams of the streamed matvec, one pair per device
-static hp_status copy_streams(cudaStream_t* in, cudaStream_t* out) {
+hp_status copy_streams(cudaStream_t* in, cudaStream_t* out) {
   static std::mutex mtx;
   static std::map<int, std::pair<cudaStream_t, cudaStream_t>> per_dev;
   int dev = 0;
