@@ -155,9 +155,9 @@ def build_set(hp, w):
     return hp.build_full(w.dim, w.bound) if w.kind == "full" else hp.build_hyperbolic(w.dim, w.bound)
 
 
-def algorithmic_bytes(w, n):
+def algorithmic_bytes(w, n, batch=None):
     """32 B per coefficient per vector per matvec: c read once, y written once."""
-    return 32.0 * n * w.batch
+    return 32.0 * n * (w.batch if batch is None else batch)
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle port)
@@ -301,13 +301,20 @@ def gpu_arm(args, rank, world, local_rank):
     ap = w.approx(0.3 if w.name == "cfg4" else 0.0, validate=False)
 
     # inputs: the seeded workload vector (rank-local part), resident in HBM
+    # batched workloads (cfg5) partition the batch by vector across ranks: rank r
+    # takes vectors [r B / P, (r + 1) B / P); single-vector reduced sets and small cubes are
+    # replicas (every rank the whole workload)
+    part = world > 1 and sharding is None and w.batch > 1
     if sharding is not None:
         c_host = sharding.local_coefficients(W, w)
     else:
         c_host = W.coefficients(w, None if w.kind == "full" else s.indices)
+        if part:
+            b0, b1 = rank * w.batch // world, (rank + 1) * w.batch // world
+            c_host = np.ascontiguousarray(c_host[b0:b1])
     x = torch.from_numpy(c_host).to(dev)
     y = torch.empty_like(x)
-    batch = w.batch
+    batch = c_host.shape[0] if part else w.batch
     nvec_local = n_local * batch
 
     def step_dev():
@@ -340,11 +347,16 @@ def gpu_arm(args, rank, world, local_rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_max = float(t)
     ms_step = ms_max / args.steps
-    total_coeffs = (sharding.global_size if sharding is not None else n_local) * batch
+    if sharding is not None:
+        total_coeffs = sharding.global_size
+    elif part:
+        total_coeffs = n_local * w.batch  # all ranks' vectors
+    else:
+        total_coeffs = n_local * batch * world  # replicas: every rank did the whole workload
     value = total_coeffs / (ms_step * 1e-3)
 
     # roofline of the matvec on this GPU: algorithmic bytes / step time
-    alg_bytes = algorithmic_bytes(w, n_local)
+    alg_bytes = algorithmic_bytes(w, n_local, batch)  # this rank's vectors
     achieved = alg_bytes / (ms / args.steps * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": profiled_traffic(args.workload),
@@ -401,14 +413,15 @@ def gpu_arm(args, rank, world, local_rank):
     if rank == 0:
         line = {"metric": "Galerkin matvec throughput", "value": value, "unit": "coeffs/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-                "higher_is_better": True, "scaling": "strong" if sharding is not None or world == 1 else "weak",
+                "higher_is_better": True,
+                "scaling": "strong" if sharding is not None or part or world == 1 else "weak",
                 "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, SURVEY.md §8(d))",
-                "config": {"workload": w.name, "set": f"{w.kind} N={w.dim} bound={w.bound}", "n": total_coeffs // batch,
-                           "batch": batch, "nterms": int(ap.nterms), "halfwidth": W.HALFWIDTH,
+                "config": {"workload": w.name, "set": f"{w.kind} N={w.dim} bound={w.bound}", "n": sharding.global_size if sharding is not None else n_local,
+                           "batch": w.batch, "nterms": int(ap.nterms), "halfwidth": W.HALFWIDTH,
                            "l2": "inputs larger than L2 (no flush)" if alg_bytes / 2 > 126e6 else
                            "working set L2-resident (not flushed)",
                            "parallelism": f"slab-j1 x{world}" if sharding is not None else
-                           ("single" if world == 1 else f"replicas x{world}")},
+                           ("single" if world == 1 else f"batch/{world}" if part else f"replicas x{world}")},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
