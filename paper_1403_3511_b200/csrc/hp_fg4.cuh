@@ -17,14 +17,8 @@
 // 64 B fills + 168 B loads, against 80 + 200 for k_fg_single.
 #pragma once
 
-#ifndef Q_NC
-#define Q_NC 0
-#endif
 #ifndef Q_CONST
-#define Q_CONST (Q_NC ? 1 : 0)
-#endif
-#ifndef Q_WREG
-#define Q_WREG 0
+#define Q_CONST 0
 #endif
 #ifndef Q_FENCES
 #define Q_FENCES 1
@@ -44,22 +38,6 @@ constexpr int Q_MAXN = 128;  // largest side the weight tables are sized for (la
 constexpr int Q_H = FG_K;
 constexpr int Q_NT = 256;
 constexpr int Q_POINTS = Q_T1 * Q_T2 * Q_T3;
-#if Q_NC
-// Q_NC ("no corners"): A1 = [axis 1 +-4][axis 2][axis 3] (256 B rows) and the +-4 columns along
-// axis 3 for the 8 tile rows only ([8][8][4] boxes): 3584 double2 = 56 KB per stage instead of
-// 64 KB (the A1 box's [+-4 rows] x [+-4 columns] corners are never read)
-constexpr int Q_CX = 0;                              // axis-3 offset of column 0 in an A1 row
-constexpr int Q_RW = Q_T3;                           // A1 row length: 16
-constexpr int Q_R1 = Q_T2 * Q_RW;                    // 128
-constexpr int Q_A1 = (Q_T1 + 2 * Q_H) * Q_R1;        // 2048
-constexpr int Q_H3 = Q_T1 * Q_T2 * Q_H;              // 256 per side
-constexpr int Q_OFF_H3LO = Q_A1, Q_OFF_H3HI = Q_A1 + Q_H3;
-constexpr int Q_B2R1 = Q_H * Q_T3;                   // B2 axis-1 stride: 64
-constexpr int Q_B2 = Q_T1 * Q_B2R1;                  // 512
-constexpr int Q_OFF_LO = Q_A1 + 2 * Q_H3, Q_OFF_HI = Q_OFF_LO + Q_B2;
-constexpr int Q_STAGE = Q_OFF_HI + Q_B2;             // 3584 double2 = 56 KB
-#else
-constexpr int Q_CX = Q_H;
 constexpr int Q_RW = Q_T3 + 2 * Q_H;                 // A1 row (axis 3) length: 24
 constexpr int Q_R1 = Q_T2 * Q_RW;                    // A1 axis-1 stride: 192
 constexpr int Q_A1 = (Q_T1 + 2 * Q_H) * Q_R1;        // 3072
@@ -67,7 +45,6 @@ constexpr int Q_B2R1 = Q_H * Q_T3;                   // B2 axis-1 stride: 64
 constexpr int Q_B2 = Q_T1 * Q_B2R1;                  // 512
 constexpr int Q_OFF_LO = Q_A1, Q_OFF_HI = Q_A1 + Q_B2;
 constexpr int Q_STAGE = Q_A1 + 2 * Q_B2;             // 4096 double2 = 64 KB
-#endif
 constexpr unsigned Q_STAGE_BYTES = Q_STAGE * 16u;
 #ifndef Q_STAGES
 #define Q_STAGES 3
@@ -79,7 +56,7 @@ constexpr size_t Q_TOFF = Q_WOFF + (Q_CONST ? 0 : (size_t)Q_MAXN * F1_WROW * siz
 constexpr size_t Q_T2OFF = Q_TOFF + (Q_CONST ? 0 : (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double));
 constexpr size_t Q_T3OFF = Q_T2OFF + (Q_CONST ? 0 : (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double));
 constexpr int Q_T3N = Q_MAXN + 16;  // axis-3 table: [5][Q_T3N], transposed (16 lanes read 128 B)
-constexpr size_t Q_BOFF = Q_T3OFF + (Q_NC ? 0 : (size_t)5 * Q_T3N * sizeof(double));
+constexpr size_t Q_BOFF = Q_T3OFF + (size_t)5 * Q_T3N * sizeof(double);
 constexpr int Q_TC = 64;  // tile codes cached in shared memory
 constexpr size_t Q_SMEM = Q_BOFF + 2 * Q_S * sizeof(uint64_t) + (Q_S + Q_TC) * sizeof(int);
 
@@ -125,21 +102,11 @@ __device__ __forceinline__ void q_table_entry(double* out, int i, const double* 
   }
   out[i] = w;
 }
-// out[0, Q_CW_N): the constant-bank tables; out[Q_CW_N + i * Q_T3N + r] = P3(r, d_i) for
-// d = -4, -2, 2, 4, 0 (the axis-3 table of the Q_NC layout, read through L1)
 template <int NMIX>
 __global__ void k_fg_qtables(double* __restrict__ out, const double* __restrict__ P, const double* __restrict__ G,
-                             const double* __restrict__ B0, int n0, int n1, int n2, int n3) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q_CW_N + 5 * Q_T3N; i += gridDim.x * blockDim.x) {
-    if (i < Q_CW_N) {
-      q_table_entry<NMIX>(out, i, P, G, B0, n0, n1, n2);
-    } else {
-      const int k = (i - Q_CW_N) / Q_T3N, r = (i - Q_CW_N) % Q_T3N;
-      const int ds[5] = {-4, -2, 2, 4, 0};
-      const double* P3 = P + 3 * FG_MAXN * FG_W;
-      out[i] = r < n3 ? P3[r * FG_W + ds[k] + FG_K] : 0.0;
-    }
-  }
+                             const double* __restrict__ B0, int n0, int n1, int n2) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q_CW_N; i += gridDim.x * blockDim.x)
+    q_table_entry<NMIX>(out, i, P, G, B0, n0, n1, n2);
 }
 
 __device__ __forceinline__ void q_prefetch4(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
@@ -152,7 +119,7 @@ __device__ __forceinline__ void q_prefetch4(const CUtensorMap* m, int c0, int c1
 template <int NMIX, bool DOT>
 __global__ void __launch_bounds__(Q_NT, 1)
     k_fg_quad(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB2,
-              const __grid_constant__ CUtensorMap mH3, const double* __restrict__ T3g, const double2* __restrict__ v, double2* __restrict__ y, const double* __restrict__ P,
+              const double2* __restrict__ v, double2* __restrict__ y, const double* __restrict__ P,
               const double* __restrict__ G, const double* __restrict__ B0, const int* __restrict__ tiles, int ntiles,
               int n0, int n1, int n2, int n3, double2* __restrict__ dotp, int exp, int plo, int phi) {
   extern __shared__ __align__(128) unsigned char q_smem[];
@@ -220,7 +187,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
   }
 #endif
   // axis-3 columns, transposed: T3w[i][r] = P3(r, -4, -2, 2, 4, 0 for i = 0..4)
-  for (int r = tid; r < (Q_NC ? 0 : Q_T3N); r += Q_NT) {
+  for (int r = tid; r < Q_T3N; r += Q_NT) {
     const bool ok = r < n3;
     T3w[0 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K - 4] : 0.0;
     T3w[1 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K - 2] : 0.0;
@@ -249,13 +216,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
     uint64_t* bar = &full[ps];
     f1_mbar_expect(bar, Q_STAGE_BYTES);
     const uint64_t pol = f1_policy(2);
-#if Q_NC
-    f1_tma4_hint(dst, &mA1, 2 * T3, T2, T1 - Q_H, pp, bar, pol);
-    f1_tma4_hint(dst + Q_OFF_H3LO, &mH3, 2 * (T3 - Q_H), T2, T1, pp, bar, pol);
-    f1_tma4_hint(dst + Q_OFF_H3HI, &mH3, 2 * (T3 + Q_T3), T2, T1, pp, bar, pol);
-#else
     f1_tma4_hint(dst, &mA1, 2 * (T3 - Q_H), T2, T1 - Q_H, pp, bar, pol);
-#endif
     f1_tma4_hint(dst + Q_OFF_LO, &mB2, 2 * T3, T2 - Q_H, T1, pp, bar, pol);
     f1_tma4_hint(dst + Q_OFF_HI, &mB2, 2 * T3, T2 + Q_T2, T1, pp, bar, pol);
   };
@@ -264,11 +225,11 @@ __global__ void __launch_bounds__(Q_NT, 1)
   int kk = 0;  // this thread's item index
 
   // centre of point (a, b) in A1; the other three points are +2 rows along axes 1 / 2
-  const int oc = (a + Q_H) * Q_R1 + b * Q_RW + c + Q_CX;
+  const int oc = (a + Q_H) * Q_R1 + b * Q_RW + c + Q_H;
   // axis-2 taps of row r (= a or a + 2) at axis-2 index t: A1 inside the tile, B2 boxes outside
   auto o2 = [&](int r, int t) {
     return t < 0 ? Q_OFF_LO + r * Q_B2R1 + (t + Q_H) * Q_T3 + c
-                 : (t >= Q_T2 ? Q_OFF_HI + r * Q_B2R1 + (t - Q_T2) * Q_T3 + c : (r + Q_H) * Q_R1 + t * Q_RW + c + Q_CX);
+                 : (t >= Q_T2 ? Q_OFF_HI + r * Q_B2R1 + (t - Q_T2) * Q_T3 + c : (r + Q_H) * Q_R1 + t * Q_RW + c + Q_H);
   };
   // per thread, fixed over the whole run: t = b-4, b-2, b+4, b+6 for rows a and a+2
   // (row a + 2 = row a + 2 axis-1 strides: 2 Q_R1 in A1, 2 Q_B2R1 in the B2 boxes)
@@ -292,29 +253,6 @@ __global__ void __launch_bounds__(Q_NT, 1)
     const bool in00 = okc && J1 < n1 && J2 < n2, in10 = okc && J1 + 2 < n1 && J2 < n2;
     const bool in01 = okc && J1 < n1 && J2 + 2 < n2, in11 = okc && J1 + 2 < n1 && J2 + 2 < n2;
     const int col = (J1 * n2 + J2) * n3 + J3;  // n1 n2 n3 <= 2^24
-    // Q_WREG: band weights held in registers for the whole tile march instead of per-plane
-    // shared loads (bit 0: axis 1, bit 1: axis 2, bit 2: axis 3)
-#if Q_WREG & 1
-    double r1a[7], r1b[7];
-#pragma unroll
-    for (int i = 0; i < 7; ++i) {
-      r1a[i] = T1w[J1 * Q_T1W + i];
-      r1b[i] = T1w[J1 * Q_T1W + 2 * Q_T1W + i];
-    }
-#endif
-#if Q_WREG & 2
-    double r2a[5], r2b[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      r2a[i] = T2w[J2 * Q_T1W + i];
-      r2b[i] = T2w[J2 * Q_T1W + 2 * Q_T1W + i];
-    }
-#endif
-#if Q_WREG & 4
-    double r3[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) r3[i] = T3w[i * Q_T3N + J3];
-#endif
     // y (and v for DOT) at plane p - 4 of the step about to run, advanced by one plane per step
     double2* yq = y + col + (int64_t)(ps0 - Q_H) * plane;
     const double2* vqp = v + col + (int64_t)(ps0 - Q_H) * plane;
@@ -348,13 +286,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
           f1_mbar_wait(&full[cs], (unsigned)(cu & 1));
           const double2* st = stg + (size_t)cs * Q_STAGE;
           // march-axis weights of plane p (uniform over the CTA)
-#if Q_NC
-#define Q3(i) __ldg(T3g + (i) * Q_T3N + J3)
-#elif Q_WREG & 4
-#define Q3(i) r3[i]
-#else
 #define Q3(i) A3[(i) * Q_T3N]
-#endif
 #if Q_CONST
 #define QW(i) q_cw[Q_CW_W + p * 8 + (i)]
 #define QT1A(i) q_cw[Q_CW_T1 + J1 * 8 + (i)]
@@ -363,20 +295,10 @@ __global__ void __launch_bounds__(Q_NT, 1)
 #define QT2B(i) q_cw[Q_CW_T2 + J2 * 8 + 16 + (i)]
 #else
 #define QW(i) W[p * F1_WROW + (i)]
-#if Q_WREG & 1
-#define QT1A(i) r1a[i]
-#define QT1B(i) r1b[i]
-#else
 #define QT1A(i) T1w[J1 * Q_T1W + (i)]
 #define QT1B(i) T1w[J1 * Q_T1W + 2 * Q_T1W + (i)]
-#endif
-#if Q_WREG & 2
-#define QT2A(i) r2a[i]
-#define QT2B(i) r2b[i]
-#else
 #define QT2A(i) T2w[J2 * Q_T1W + (i)]
 #define QT2B(i) T2w[J2 * Q_T1W + 2 * Q_T1W + (i)]
-#endif
 #endif
           const double2 wa = make_double2(QW(0), QW(1));
           const double2 wc = make_double2(QW(4), QW(5));
@@ -485,17 +407,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const int o = oc + (k & 1) * 2 * Q_R1 + (k >> 1) * 2 * Q_RW;
-#if Q_NC
-            // columns off the tile come from the [8][8][4] axis-3 halo boxes
-            const int hrow = ((a + 2 * (k & 1)) * Q_T2 + b + 2 * (k >> 1)) * Q_H;
-            auto off3 = [&](int d) {
-              const int t = c + d;
-              return t < 0 ? Q_OFF_H3LO + hrow + t + Q_H : (t >= Q_T3 ? Q_OFF_H3HI + hrow + t - Q_T3 : o + d);
-            };
-            const double2 t0 = st[off3(-4)], t1 = st[off3(-2)], t2 = st[off3(2)], t3 = st[off3(4)];
-#else
             const double2 t0 = st[o - 4], t1 = st[o - 2], t2 = st[o + 2], t3 = st[o + 4];
-#endif
             fma2(w3[0], t0, R[k][U]);
             fma2(w3[1], t1, R[k][U]);
             fma2(w3[2], t2, R[k][U]);

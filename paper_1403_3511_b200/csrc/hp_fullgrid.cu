@@ -325,9 +325,7 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
   *launched = false;
   CUtensorMap mA1, mB2;
   if (fg_quad() && s->side[0] <= Q_MAXN && s->side[1] <= Q_MAXN) {
-    CUtensorMap mH3;
-    if (!tma_map(&mA1, v, s->side, 2 * Q_RW, Q_T2, Q_T1 + 2 * Q_H) || !tma_map(&mB2, v, s->side, 2 * Q_T3, Q_H, Q_T1) ||
-        !tma_map(&mH3, v, s->side, 2 * Q_H, Q_T2, Q_T1))
+    if (!tma_map(&mA1, v, s->side, 2 * Q_RW, Q_T2, Q_T1 + 2 * Q_H) || !tma_map(&mB2, v, s->side, 2 * Q_T3, Q_H, Q_T1))
       return HP_OK;
     hp_status rc = make_tiles(s, Q_T1, Q_T2, Q_T3, &s->fg_tiles4, &s->fg_ntiles4);
     if (rc) return rc;
@@ -352,12 +350,11 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
       if (dev < 0 || dev >= 64) return HP_ERR_CUDA;
       if (!q_ev[dev]) {
         HP_CUDA(cudaEventCreateWithFlags(&q_ev[dev], cudaEventDisableTiming));
-        HP_CUDA(cudaMalloc(&q_stage[dev], (Q_CW_N + 5 * Q_T3N) * sizeof(double)));
+        HP_CUDA(cudaMalloc(&q_stage[dev], Q_CW_N * sizeof(double)));
       } else {
         HP_CUDA(cudaStreamWaitEvent(st, q_ev[dev], 0));
       }
-      k_fg_qtables<NMIX><<<(Q_CW_N + 5 * Q_T3N + 255) / 256, 256, 0, st>>>(q_stage[dev], P, G, B0, n0, s->side[1],
-                                                                          s->side[2], s->side[3]);
+      k_fg_qtables<NMIX><<<(Q_CW_N + 255) / 256, 256, 0, st>>>(q_stage[dev], P, G, B0, n0, s->side[1], s->side[2]);
       HP_LAUNCH_CHECK("k_fg_qtables");
       HP_CUDA(cudaMemcpyToSymbolAsync(q_cw, q_stage[dev], Q_CW_N * sizeof(double), 0, cudaMemcpyDeviceToDevice, st));
     }
@@ -372,7 +369,7 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
       *launched = true;
       return HP_OK;
     }
-    kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, mH3, Q_NC ? q_stage[dev] + Q_CW_N : nullptr, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
+    kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
                                      s->side[2], s->side[3], use_dot ? dot->partial : nullptr, fg_exp(), plo, phi);
     HP_LAUNCH_CHECK("k_fg_quad");
     if (Q_CONST) HP_CUDA(cudaEventRecord(q_ev[dev], st));
