@@ -110,7 +110,7 @@ struct FgPlan {
 
 static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch, int flags) {
   FgPlan P;
-  if (!s->boxed || s->dim != 4 || dtype != HP_C128 || batch != 1) return P;
+  if (!s->boxed || s->dim != 4 || dtype != HP_C128 || batch < 1) return P;
   for (int a = 0; a < 4; ++a) if (s->side[a] > FG_MAXN) return P;
   if (((int64_t)s->side[2] * s->side[3]) % FG_C != 0) return P;
   if (s->side[1] * FG_C > 512 || s->side[3] > 128) return P;
@@ -513,17 +513,22 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   const double2* v = (const double2*)in;
   double2* y = (double2*)out;
   const bool even = F.mask[0] == FG_MASK_EVEN && F.mask[2] == FG_MASK_EVEN && F.mask[3] == FG_MASK_EVEN;
-  // single pass for the even-band class (cfg4)
+  // single pass for the even-band class (cfg4); a batch runs one launch per vector
   if (fg_single_class(F)) {
     bool launched = false;
-    rc = F.nmix ? launch_single<1>(s, v, y, P, G, F, st, dot, &launched)
-                : launch_single<0>(s, v, y, P, G, F, st, dot, &launched);
-    if (rc) return rc;
+    for (int64_t b = 0; b < batch; ++b) {
+      const int64_t off = b * s->n;
+      rc = F.nmix ? launch_single<1>(s, v + off, y + off, P, G, F, st, batch == 1 ? dot : nullptr, &launched)
+                  : launch_single<0>(s, v + off, y + off, P, G, F, st, batch == 1 ? dot : nullptr, &launched);
+      if (rc) return rc;
+      if (!launched) break;
+    }
     if (launched) {
       *done = true;
       return HP_OK;
     }
   }
+  if (batch != 1) return HP_OK;  // the two-pass kernels take one vector: level evaluator
   // pass B
   rc = even ? launch_inner<FG_MASK_EVEN, FG_MASK_EVEN>(s, v, u, P, st)
             : launch_inner<FG_MASK_ALL, FG_MASK_ALL>(s, v, u, P, st);
