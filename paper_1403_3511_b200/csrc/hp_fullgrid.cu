@@ -317,66 +317,88 @@ static int sm_count() {
   return n;
 }
 
+// The constant-bank weight tables (k_fg_quad with Q_CONST, k_fg_quad_ri) live in one per-device
+// buffer: their launches are serialised across streams -- each waits for the previous user's
+// kernel before the tables are overwritten.  The lock is held from staging to the launch.
+struct ConstTables {
+  std::unique_lock<std::mutex> lk;
+  cudaEvent_t done = nullptr;  // recorded after the kernel that reads the tables
+};
+template <int NMIX>
+static hp_status stage_const_tables(const hp_set_s* s, const double* P, const double* G, const double* B0,
+                                    cudaStream_t st, ConstTables* ct) {
+  static std::mutex mtx;
+  static cudaEvent_t ev[64] = {};
+  static double* stage[64] = {};
+  ct->lk = std::unique_lock<std::mutex>(mtx);
+  int dev = 0;
+  HP_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return HP_ERR_CUDA;
+  if (!ev[dev]) {
+    HP_CUDA(cudaEventCreateWithFlags(&ev[dev], cudaEventDisableTiming));
+    HP_CUDA(cudaMalloc(&stage[dev], Q_CW_N * sizeof(double)));
+  } else {
+    HP_CUDA(cudaStreamWaitEvent(st, ev[dev], 0));
+  }
+  k_fg_qtables<NMIX><<<(Q_CW_N + 255) / 256, 256, 0, st>>>(stage[dev], P, G, B0, s->side[0], s->side[1], s->side[2]);
+  HP_LAUNCH_CHECK("k_fg_qtables");
+  HP_CUDA(cudaMemcpyToSymbolAsync(q_cw, stage[dev], Q_CW_N * sizeof(double), 0, cudaMemcpyDeviceToDevice, st));
+  ct->done = ev[dev];
+  return HP_OK;
+}
+
+// k_fg_quad (default) or k_fg_quad_ri (HP_FG_RI=1): 8 x 8 x 16 tiles, sides <= Q_MAXN
+template <int NMIX>
+static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, const double* P, const double* G,
+                             const FgPlan& F, cudaStream_t st, DotOut* dot, bool* launched, int plo, int phi) {
+  CUtensorMap mA1, mB2;
+  if (!tma_map(&mA1, v, s->side, 2 * Q_RW, Q_T2, Q_T1 + 2 * Q_H) || !tma_map(&mB2, v, s->side, 2 * Q_T3, Q_H, Q_T1))
+    return HP_OK;  // no driver entry point: the two-pass kernels run
+  hp_status rc = make_tiles(s, Q_T1, Q_T2, Q_T3, &s->fg_tiles4, &s->fg_ntiles4);
+  if (rc) return rc;
+  const int n0 = s->side[0];
+  const double* B0 = s->fg_basis + (size_t)(NMIX ? F.r0[0] : 0) * n0 * FG_W;  // axis 0, degree r0
+  const int grid = std::min(s->fg_ntiles4, sm_count());
+  const bool use_dot = dot && dot->partial && grid <= dot->capacity;
+  double2* dotp = use_dot ? dot->partial : nullptr;
+  const bool ri = fg_ri();
+  ConstTables ct;
+  if (Q_CONST || ri) {
+    if ((rc = stage_const_tables<NMIX>(s, P, G, B0, st, &ct))) return rc;
+  }
+  if (ri) {
+    auto kern = use_dot ? k_fg_quad_ri<NMIX, true> : k_fg_quad_ri<NMIX, false>;
+    HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM));
+    kern<<<grid, QR_NT, QR_SMEM, st>>>(mA1, mB2, v, y, P, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1], s->side[2],
+                                        s->side[3], dotp, plo, phi);
+    HP_LAUNCH_CHECK("k_fg_quad_ri");
+  } else {
+    auto kern = use_dot ? k_fg_quad<NMIX, true> : k_fg_quad<NMIX, false>;
+    HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
+    // exp = 0: k_fg_quad keeps the experiment slot of k_fg_single's signature (dropping it moves
+    // ptxas to a spilling allocation of the 255-register kernel)
+    kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
+                                     s->side[2], s->side[3], dotp, 0, plo, phi);
+    HP_LAUNCH_CHECK("k_fg_quad");
+  }
+  if (ct.done) HP_CUDA(cudaEventRecord(ct.done, st));
+  if (use_dot) dot->n = grid;
+  *launched = true;
+  return HP_OK;
+}
+
+// the single-pass evaluator of the cfg4 class (output planes [plo, phi)): k_fg_quad, or
+// k_fg_single on cubes with a side > Q_MAXN (HP_FG_QUAD=0 forces it); *launched stays false
+// when TMA descriptors are unavailable (the caller then runs the two-pass kernels)
 template <int NMIX>
 static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, const double* P, const double* G,
                                const FgPlan& F, cudaStream_t st, DotOut* dot, bool* launched, int plo = 0,
                                int phi = -1) {
   if (phi < 0) phi = s->side[0];
   *launched = false;
+  if (fg_quad() && s->side[0] <= Q_MAXN && s->side[1] <= Q_MAXN)
+    return launch_quad<NMIX>(s, v, y, P, G, F, st, dot, launched, plo, phi);
   CUtensorMap mA1, mB2;
-  if (fg_quad() && s->side[0] <= Q_MAXN && s->side[1] <= Q_MAXN) {
-    if (!tma_map(&mA1, v, s->side, 2 * Q_RW, Q_T2, Q_T1 + 2 * Q_H) || !tma_map(&mB2, v, s->side, 2 * Q_T3, Q_H, Q_T1))
-      return HP_OK;
-    hp_status rc = make_tiles(s, Q_T1, Q_T2, Q_T3, &s->fg_tiles4, &s->fg_ntiles4);
-    if (rc) return rc;
-    const int n0 = s->side[0];
-    const double* B0 = s->fg_basis + (size_t)(NMIX ? F.r0[0] : 0) * n0 * FG_W;
-    const int grid = std::min(s->fg_ntiles4, sm_count());
-    const bool use_dot = dot && dot->partial && grid <= dot->capacity;
-    auto kern = use_dot ? k_fg_quad<NMIX, true> : k_fg_quad<NMIX, false>;
-    HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
-    // the weight tables of the constant-bank variants live in one per-device constant buffer:
-    // launches that use it are serialised across streams (each waits for the previous user's
-    // kernel before overwriting)
-    static std::mutex q_mtx;
-    static cudaEvent_t q_ev[64] = {};
-    static double* q_stage[64] = {};
-    std::unique_lock<std::mutex> lk(q_mtx, std::defer_lock);
-    int dev = 0;
-    const bool ri = fg_ri();
-    if (Q_CONST || ri) {
-      lk.lock();
-      HP_CUDA(cudaGetDevice(&dev));
-      if (dev < 0 || dev >= 64) return HP_ERR_CUDA;
-      if (!q_ev[dev]) {
-        HP_CUDA(cudaEventCreateWithFlags(&q_ev[dev], cudaEventDisableTiming));
-        HP_CUDA(cudaMalloc(&q_stage[dev], Q_CW_N * sizeof(double)));
-      } else {
-        HP_CUDA(cudaStreamWaitEvent(st, q_ev[dev], 0));
-      }
-      k_fg_qtables<NMIX><<<(Q_CW_N + 255) / 256, 256, 0, st>>>(q_stage[dev], P, G, B0, n0, s->side[1], s->side[2]);
-      HP_LAUNCH_CHECK("k_fg_qtables");
-      HP_CUDA(cudaMemcpyToSymbolAsync(q_cw, q_stage[dev], Q_CW_N * sizeof(double), 0, cudaMemcpyDeviceToDevice, st));
-    }
-    if (ri) {
-      auto kr = use_dot ? k_fg_quad_ri<NMIX, true> : k_fg_quad_ri<NMIX, false>;
-      HP_CUDA(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM));
-      kr<<<grid, QR_NT, QR_SMEM, st>>>(mA1, mB2, v, y, P, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1], s->side[2],
-                                        s->side[3], use_dot ? dot->partial : nullptr, plo, phi);
-      HP_LAUNCH_CHECK("k_fg_quad_ri");
-      HP_CUDA(cudaEventRecord(q_ev[dev], st));
-      if (use_dot) dot->n = grid;
-      *launched = true;
-      return HP_OK;
-    }
-    kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
-                                     s->side[2], s->side[3], use_dot ? dot->partial : nullptr, fg_exp(), plo, phi);
-    HP_LAUNCH_CHECK("k_fg_quad");
-    if (Q_CONST) HP_CUDA(cudaEventRecord(q_ev[dev], st));
-    if (use_dot) dot->n = grid;
-    *launched = true;
-    return HP_OK;
-  }
   if (!tma_map(&mA1, v, s->side, 2 * F1_RW, F1_T2, F1_T1 + 2 * F1_H) ||
       !tma_map(&mB2, v, s->side, 2 * F1_T3, F1_H, F1_T1))
     return HP_OK;  // no driver entry point: the two-pass kernels run
