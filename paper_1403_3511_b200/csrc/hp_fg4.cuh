@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
     double2* dst = stg + (size_t)ps * Q_STAGE;
     uint64_t* bar = &full[ps];
     f1_mbar_expect(bar, Q_STAGE_BYTES);
-    const uint64_t pol = f1_policy(2);
+    const uint64_t pol = f1_policy((exp >> 4) & 3 ? (exp >> 4) & 3 : 2);  // HP_FG_EXP bits 4-5: L2 policy experiments
     f1_tma4_hint(dst, &mA1, 2 * (T3 - Q_H), T2, T1 - Q_H, pp, bar, pol);
     f1_tma4_hint(dst + Q_OFF_LO, &mB2, 2 * T3, T2 - Q_H, T1, pp, bar, pol);
     f1_tma4_hint(dst + Q_OFF_HI, &mB2, 2 * T3, T2 + Q_T2, T1, pp, bar, pol);

@@ -378,7 +378,7 @@ static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, co
     // exp = 0: k_fg_quad keeps the experiment slot of k_fg_single's signature (dropping it moves
     // ptxas to a spilling allocation of the 255-register kernel)
     kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
-                                     s->side[2], s->side[3], dotp, 0, plo, phi);
+                                     s->side[2], s->side[3], dotp, fg_exp(), plo, phi);
     HP_LAUNCH_CHECK("k_fg_quad");
   }
   if (ct.done) HP_CUDA(cudaEventRecord(ct.done, st));
