@@ -43,16 +43,19 @@ def main():
     fh.propagate(scheme, y, 0.0, w.dt, 1, args.m)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0 = time.perf_counter()
-    e0.record()
-    yT = fh.propagate(scheme, y, 0.0, w.dt, nsteps, args.m)
-    e1.record()
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
+    from bench import ClockSampler
+
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0 = time.perf_counter()
+        e0.record()
+        yT = fh.propagate(scheme, y, 0.0, w.dt, nsteps, args.m)
+        e1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
     dev_ms = e0.elapsed_time(e1) / nsteps
     out = {"workload": w.name, "n": s.size, "steps": nsteps, "dt": w.dt, "m": args.m,
            "device_ms_per_step": round(dev_ms, 4), "wall_ms_per_step": round(wall * 1e3 / nsteps, 4),
-           "algorithmic_bytes_per_step": (112 * args.m - 48) * s.size}
+           "algorithmic_bytes_per_step": (112 * args.m - 48) * s.size, "clocks": clk.summary()}
     out["achieved_GBs"] = round(out["algorithmic_bytes_per_step"] / (dev_ms * 1e-3) / 1e9, 1)
     # CPU oracle on the first cpu_steps steps, same inputs
     k = min(args.cpu_steps, nsteps)
