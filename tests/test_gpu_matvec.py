@@ -358,6 +358,31 @@ def test_cfg4_full_size_slab_vs_oracle(hp):
     assert float(torch.linalg.vector_norm(y2 - 2.0 * y) / torch.linalg.vector_norm(y)) < 1e-14
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+def test_full_size_reduced_sets_vs_reference_order(hp, name):
+    """Full-size cfg3 (3.6e7) / cfg5 (2.6e7) matvecs: the default level evaluator (line-blocked
+    axis-1 order, batch) against the device run of the reference's own evaluation order --
+    the program that is bitwise equal to the reference on every golden case -- within 1e-12;
+    batched equals per-vector bit for bit; linearity."""
+    import torch
+
+    w = W.CONFIGS[name]
+    s = hp.build_hyperbolic(w.dim, w.bound)
+    ap = w.approx(0.0)
+    appl = hp.get_applier(s)
+    gen = np.random.default_rng(7)
+    V = torch.from_numpy(gen.standard_normal((2, s.size)) + 1j * gen.standard_normal((2, s.size))).cuda()
+    Y = appl.apply_polynomial(ap, V)
+    for b in range(2):
+        yb = appl.apply_polynomial(ap, V[b].contiguous())
+        assert torch.equal(Y[b], yb)
+        yr = appl.apply_polynomial(ap, V[b].contiguous(), ref_order=True)
+        assert float(torch.linalg.vector_norm(yb - yr) / torch.linalg.vector_norm(yr)) < TOL
+    y2 = appl.apply_polynomial(ap, (V[0] * (0.5 - 2.0j)).contiguous())
+    assert float(torch.linalg.vector_norm(y2 - (0.5 - 2.0j) * Y[0]) / torch.linalg.vector_norm(y2)) < 1e-14
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_slab_shards_on_device(hp, world):
     """All ranks' slab shards in one process: device slab sets + the halo plan reproduce
