@@ -202,6 +202,16 @@ hp_status hp_cdot(int64_t n, const void* a_dev, const void* b_dev, double* out_d
 /* out_dev[0] = ||a||_2 (complex128 vector), fixed summation order */
 hp_status hp_cnrm2(int64_t n, const void* a_dev, double* out_dev, void* workspace_dev,
                    void* stream);
+/* Slab-sharded Lanczos (krylov_propagator.py:86-89): out = a x + b y + c z
+   (real a, b, c; z may be NULL) and norm2_dev[0] = ||out||^2 of this rank's part (fixed order;
+   the caller sums ranks).  workspace: hp_reduce_workspace_bytes(n). */
+hp_status hp_lincomb3_nrm2sq(int64_t n, double a, const void* x_dev, double b, const void* y_dev, double c,
+                             const void* z_dev, void* out_dev, double* norm2_dev, void* workspace_dev,
+                             void* stream);
+/* out = sum_k coef[k] V_k, complex coefficients coef_host[2k], coef_host[2k+1] (m <= 32):
+   the basis combine of lanczos_exp_apply (krylov_propagator.py:180-186) */
+hp_status hp_lincomb(int64_t n, int m, const void* const* vecs_host, const double* coef_host, void* out_dev,
+                     void* stream);
 
 #ifdef __cplusplus
 }

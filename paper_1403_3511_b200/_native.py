@@ -69,6 +69,9 @@ SIGNATURES = {
     "hp_reduce_workspace_bytes": (c_sz, [c_i64]),
     "hp_cdot": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "hp_cnrm2": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "hp_lincomb3_nrm2sq": (c_int, [c_i64, ctypes.c_double, c_vp, ctypes.c_double, c_vp, ctypes.c_double, c_vp, c_vp,
+                                   c_vp, c_vp, c_vp]),
+    "hp_lincomb": (c_int, [c_i64, ctypes.c_int, c_vp, c_vp, c_vp, c_vp]),
 }
 
 

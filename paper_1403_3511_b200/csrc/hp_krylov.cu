@@ -516,11 +516,87 @@ static hp_status check_m(int m) {
 
 using namespace hp;
 
+// ---------------------------------------------------------------- sharded Lanczos building blocks
+
+// out = a x + b y + c z (z optional) with the per-block partial sums of ||out||^2: the update
+// r = A v_k - alpha_k v_k - beta_{k-1} v_{k-1} (krylov_propagator.py:86-89) on one rank's owned
+// planes, its norm reduced across ranks by the caller (sharding.sharded_propagate)
+__global__ void __launch_bounds__(HP_RED_THREADS) k_lincomb3_part(int64_t n, double a, const double2* __restrict__ x,
+                                                                  double b, const double2* __restrict__ y, double c,
+                                                                  const double2* __restrict__ z,
+                                                                  double2* __restrict__ out,
+                                                                  double2* __restrict__ partial) {
+  __shared__ double2 sh[HP_RED_THREADS];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 xv = __ldg(x + i), yv = __ldg(y + i);
+    double2 r = make_double2(fma(b, yv.x, a * xv.x), fma(b, yv.y, a * xv.y));
+    if (z) {
+      const double2 zv = __ldg(z + i);
+      r.x = fma(c, zv.x, r.x);
+      r.y = fma(c, zv.y, r.y);
+    }
+    out[i] = r;
+    acc.x = fma(r.x, r.x, fma(r.y, r.y, acc.x));
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = HP_RED_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = cadd(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+constexpr int HP_LINCOMB_MAX = 32;
+struct LinCombArgs {
+  const double2* v[HP_LINCOMB_MAX];
+  double2 c[HP_LINCOMB_MAX];
+  int m;
+};
+// out = sum_k c_k V_k: the basis combine of lanczos_exp_apply (krylov_propagator.py:180-186)
+__global__ void k_lincomb(int64_t n, LinCombArgs A, double2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < A.m; ++k) {
+      const double2 v = __ldg(A.v[k] + i), c = A.c[k];
+      acc.x = fma(c.x, v.x, fma(-c.y, v.y, acc.x));
+      acc.y = fma(c.x, v.y, fma(c.y, v.x, acc.y));
+    }
+    out[i] = acc;
+  }
+}
+
 extern "C" {
 
 size_t hp_reduce_workspace_bytes(int64_t n) {
   (void)n;
   return align_up(HP_RED_BLOCKS * sizeof(double2)) + align_up(sizeof(LzState));
+}
+
+hp_status hp_lincomb3_nrm2sq(int64_t n, double a, const void* x, double b, const void* y, double c, const void* z,
+                             void* out, double* norm2_out, void* ws, void* stream) {
+  if (n < 0 || !x || !y || !out || !norm2_out || !ws) return fail(HP_ERR_VALUE, "lincomb3: null buffer");
+  cudaStream_t st = as_stream(stream);
+  k_lincomb3_part<<<HP_RED_BLOCKS, HP_RED_THREADS, 0, st>>>(n, a, (const double2*)x, b, (const double2*)y, c,
+                                                             (const double2*)z, (double2*)out, (double2*)ws);
+  HP_LAUNCH_CHECK("k_lincomb3_part");
+  k_red_final<<<1, HP_RED_THREADS, 0, st>>>((double2*)ws, HP_RED_BLOCKS, nullptr, 0, 4, 0.0, norm2_out);
+  HP_LAUNCH_CHECK("k_red_final");
+  return HP_OK;
+}
+
+hp_status hp_lincomb(int64_t n, int m, const void* const* vecs, const double* coef, void* out, void* stream) {
+  if (n < 0 || m < 1 || m > HP_LINCOMB_MAX || !vecs || !coef || !out) return fail(HP_ERR_VALUE, "lincomb: bad arguments");
+  LinCombArgs A;
+  A.m = m;
+  for (int k = 0; k < m; ++k) {
+    A.v[k] = (const double2*)vecs[k];
+    A.c[k] = make_double2(coef[2 * k], coef[2 * k + 1]);
+  }
+  k_lincomb<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, A, (double2*)out);
+  HP_LAUNCH_CHECK("k_lincomb");
+  return HP_OK;
 }
 
 hp_status hp_cdot(int64_t n, const void* a, const void* b, double* out, void* ws, void* stream) {

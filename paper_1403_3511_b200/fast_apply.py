@@ -20,6 +20,7 @@ Two evaluation orders are available (see csrc/hp_apply.cu):
 from __future__ import annotations
 
 import ctypes
+from collections import OrderedDict
 import warnings
 
 import numpy as np
@@ -153,6 +154,40 @@ class PolynomialApplier:
             ctypes.c_void_p(ws.data_ptr()), ws.numel(), nat.stream_ptr()))
         return _Dev.back(out, host)
 
+    def _into_entry(self, approx, x, flags: int, batch: int):
+        """Term arrays of `approx` and a workspace for the device-resident entry points.
+
+        Term arrays are cached per (approx, shape, flags) in a small LRU (a time-dependent
+        surrogate is a new object every step); the workspace is shared by every approx of the
+        same (shape, dtype, flags, stream) and grown to the largest request, so a stepping loop
+        allocates it once instead of once per step.
+        """
+        import torch
+
+        key = (id(approx), tuple(x.shape), x.dtype, flags)
+        cache = self.__dict__.setdefault("_into_cache", OrderedDict())
+        ent = cache.get(key)
+        if ent is None or ent[0] is not approx:
+            degs, coeffs = _term_arrays(approx, self.iset.dim)
+            dtype = nat.HP_C128 if x.is_complex() else nat.HP_F64
+            h = ctypes.c_void_p(self.iset.handle)
+            wsb = int(nat.lib().hp_poly_workspace_bytes(h, degs.ctypes.data_as(nat.c_i32p), degs.shape[0], dtype,
+                                                        batch, flags))
+            ent = (approx, degs, coeffs, h, batch, dtype, wsb)
+            cache[key] = ent
+            while len(cache) > 16:
+                cache.popitem(last=False)
+        else:
+            cache.move_to_end(key)
+        dev = x.device if x.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        wkey = (tuple(x.shape), x.dtype, flags, torch.cuda.current_stream(dev).cuda_stream)
+        wss = self.__dict__.setdefault("_into_ws", {})
+        ws = wss.get(wkey)
+        if ws is None or ws.numel() < max(ent[6], 16):
+            ws = torch.empty(max(ent[6], 16), dtype=torch.uint8, device=dev)
+            wss[wkey] = ws
+        return ent[:6] + (ws,)
+
     def apply_into(self, approx, x, y, flags: int = 0) -> None:
         """Device-resident hot loop: y <- W(X) x for preallocated CUDA tensors.
 
@@ -162,20 +197,8 @@ class PolynomialApplier:
         """
         import torch
 
-        key = (id(approx), tuple(x.shape), x.dtype, flags)
-        cache = self.__dict__.setdefault("_into_cache", {})
-        ent = cache.get(key)
-        if ent is None:
-            degs, coeffs = _term_arrays(approx, self.iset.dim)
-            batch = 1 if x.dim() == 1 else x.shape[0]
-            dtype = nat.HP_C128 if x.is_complex() else nat.HP_F64
-            h = ctypes.c_void_p(self.iset.handle)
-            wsb = nat.lib().hp_poly_workspace_bytes(h, degs.ctypes.data_as(nat.c_i32p), degs.shape[0], dtype,
-                                                    batch, flags)
-            ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=x.device)
-            ent = (approx, degs, coeffs, h, batch, dtype, ws)
-            cache[key] = ent
-        _, degs, coeffs, h, batch, dtype, ws = ent
+        batch = 1 if x.dim() == 1 else x.shape[0]
+        _, degs, coeffs, h, batch, dtype, ws = self._into_entry(approx, x, flags, batch)
         nat.check(nat.lib().hp_apply_polynomial(
             h, degs.ctypes.data_as(nat.c_i32p), coeffs.ctypes.data_as(nat.c_dblp), degs.shape[0],
             float(approx.halfwidth), dtype, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), batch,
@@ -190,19 +213,8 @@ class PolynomialApplier:
         """
         import torch
 
+        _, degs, coeffs, h, _batch, dtype, ws = self._into_entry(approx, x, flags, 1)
         key = (id(approx), tuple(x.shape), x.dtype, flags)
-        cache = self.__dict__.setdefault("_into_cache", {})
-        ent = cache.get(key)
-        if ent is None:
-            degs, coeffs = _term_arrays(approx, self.iset.dim)
-            dtype = nat.HP_C128 if x.is_complex() else nat.HP_F64
-            h = ctypes.c_void_p(self.iset.handle)
-            wsb = nat.lib().hp_poly_workspace_bytes(h, degs.ctypes.data_as(nat.c_i32p), degs.shape[0], dtype, 1,
-                                                    flags)
-            ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device=x.device)
-            ent = (approx, degs, coeffs, h, 1, dtype, ws)
-            cache[key] = ent
-        _, degs, coeffs, h, _batch, dtype, ws = ent
         unsupported = self.__dict__.setdefault("_planes_unsupported", set())
         if key in unsupported:
             return False
@@ -231,22 +243,15 @@ class PolynomialApplier:
             raise ValueError("apply_host_into expects two CPU tensors of the same shape and dtype")
         if not (x_host.is_contiguous() and y_host.is_contiguous()):
             raise ValueError("apply_host_into expects contiguous tensors")
-        key = ("host", id(approx), tuple(x_host.shape), x_host.dtype, flags)
-        cache = self.__dict__.setdefault("_into_cache", {})
-        ent = cache.get(key)
-        if ent is None:
-            degs, coeffs = _term_arrays(approx, self.iset.dim)
-            batch = 1 if x_host.dim() == 1 else x_host.shape[0]
-            dtype = nat.HP_C128 if x_host.is_complex() else nat.HP_F64
-            h = ctypes.c_void_p(self.iset.handle)
-            wsb = nat.lib().hp_poly_workspace_bytes(h, degs.ctypes.data_as(nat.c_i32p), degs.shape[0], dtype,
-                                                    batch, flags)
-            ws = torch.empty(max(int(wsb), 16), dtype=torch.uint8, device="cuda")
+        batch = 1 if x_host.dim() == 1 else x_host.shape[0]
+        _, degs, coeffs, h, batch, dtype, ws = self._into_entry(approx, x_host, flags, batch)
+        # device staging buffers, shared like the workspace (per shape, dtype and stream)
+        bkey = ("host", tuple(x_host.shape), x_host.dtype, torch.cuda.current_stream().cuda_stream)
+        bufs = self.__dict__.setdefault("_into_bufs", {})
+        if bkey not in bufs:
             xd = torch.empty(x_host.shape, dtype=x_host.dtype, device="cuda")
-            yd = torch.empty_like(xd)
-            ent = (approx, degs, coeffs, h, batch, dtype, ws, xd, yd)
-            cache[key] = ent
-        _, degs, coeffs, h, batch, dtype, ws, xd, yd = ent
+            bufs[bkey] = (xd, torch.empty_like(xd))
+        xd, yd = bufs[bkey]
         nat.check(nat.lib().hp_apply_polynomial_streamed(
             h, degs.ctypes.data_as(nat.c_i32p), coeffs.ctypes.data_as(nat.c_dblp), degs.shape[0],
             float(approx.halfwidth), dtype, ctypes.c_void_p(x_host.data_ptr()), ctypes.c_void_p(y_host.data_ptr()),

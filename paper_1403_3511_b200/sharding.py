@@ -18,6 +18,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 # input planes the fused full-cube kernel reads on each side of an output plane (hp_fg1.cuh F1_H)
 RADIUS = 4
 
@@ -173,3 +175,133 @@ class SlabShard:
             appl.apply_planes_into(ap, x, y, lo, rng[0], flags)
         if hi > rng[1]:
             appl.apply_planes_into(ap, x, y, rng[1], hi, flags)
+
+
+# ---------------------------------------------------------------- sharded time stepping
+
+def dist_sum(partials):
+    """Cross-rank sum of this process's partial scalars (a device float64 tensor per local
+    shard): all-gather of the per-rank partials, then a rank-ordered sum (deterministic and
+    identical on every rank).  One local shard per process in a distributed run."""
+    total = partials[0].clone()
+    for p in partials[1:]:
+        total += p
+    return fixed_order_sum(total)
+
+
+def local_sum(partials):
+    """The cross-rank sum when every rank's shard lives in this process (tests)."""
+    total = partials[0].clone()
+    for p in partials[1:]:
+        total += p
+    return total
+
+
+def sharded_propagate(shards, fh, ys, t0: float, h: float, nsteps: int, m: int, *, reduce=dist_sum,
+                      exchange=None):
+    """Midpoint Magnus steps (krylov_propagator.py:192-263, lanczos :58-104, expm :173-186) with
+    the state split in j1-slabs: SURVEY.md §8(e).
+
+    ``shards`` are this process's SlabShard(s) (one per rank; several only when tests emulate
+    the ranks in one process), ``ys`` their box-sized complex128 device states (owned planes
+    valid, halos are refreshed by each matvec's exchange), ``fh`` the FastHamiltonian of the
+    full cube (its surrogate is re-interpolated at every step's midpoint, as the reference
+    does).  Every vector operation runs on the owned planes of each shard; Lanczos dot products
+    and norms are per-shard partials combined by ``reduce`` (all-gather + rank-ordered sum).
+
+    The basis is kept unnormalised (u_k = v_k / s_k with known s_k), so each Lanczos iteration
+    is the sharded matvec on u_k, one dot (hp_cdot) and one fused update + norm pass
+    (hp_lincomb3_nrm2sq: u_{k+1} = s_k A u_k - alpha_k s_k u_k - beta_{k-1} s_{k-1} u_{k-1});
+    the step ends with one combine pass (hp_lincomb).  Returns ``ys`` advanced in place.
+    """
+    import ctypes
+
+    import torch
+
+    from . import _native as nat
+    from .fast_apply import get_applier
+    from .krylov_propagator import _BREAKDOWN_TOL, expm_tridiag_column
+
+    L = nat.lib()
+    q = float(fh.potential.harmonic_part)
+    ns = len(shards)
+    appls = [get_applier(sh.set) for sh in shards]
+    own = [sh.geo.own_slice for sh in shards]
+    nloc = [own[i].stop - own[i].start for i in range(ns)]
+    outs = [torch.zeros_like(y) for y in ys]
+    ws = [torch.empty(int(L.hp_reduce_workspace_bytes(nloc[i])), dtype=torch.uint8, device="cuda")
+          for i in range(ns)]
+    sc = [torch.zeros(2, dtype=torch.float64, device="cuda") for _ in range(ns)]
+    vp = ctypes.c_void_p
+
+    def matvec(ap, boxes):
+        """A(t) u on the owned planes of every shard (views into `outs`); `boxes` are the
+        box-sized basis vectors (owned planes valid), whose halos the exchange fills."""
+        if exchange is None:
+            for i, sh in enumerate(shards):
+                sh.apply_polynomial(appls[i], ap, boxes[i], outs[i], nat.HP_ADD_OSC)
+        else:  # emulated ranks: one exchange over all boxes, then the local matvecs
+            exchange([sh.geo for sh in shards], boxes)
+            for i in range(ns):
+                appls[i].apply_into(ap, boxes[i], outs[i], nat.HP_ADD_OSC)
+        w = [outs[i][own[i]] for i in range(ns)]
+        if q != 0.0:
+            for i in range(ns):
+                w[i].add_(appls[i].apply_square_sum(boxes[i])[own[i]], alpha=q)
+        return w
+
+    def cdot(a, b):  # sum over ranks of a^H b -> (re, im)
+        for i in range(ns):
+            nat.check(L.hp_cdot(nloc[i], vp(a[i].data_ptr()), vp(b[i].data_ptr()), vp(sc[i].data_ptr()),
+                                vp(ws[i].data_ptr()), nat.stream_ptr()))
+        return reduce([x.clone() for x in sc]).cpu().numpy()
+
+    def update(cw, w, cu, u, cp, prev, out):  # out = cw w + cu u + cp prev; returns sum ||out||^2
+        for i in range(ns):
+            nat.check(L.hp_lincomb3_nrm2sq(nloc[i], cw, vp(w[i].data_ptr()), cu, vp(u[i].data_ptr()), cp,
+                                           vp(prev[i].data_ptr()) if prev is not None else None,
+                                           vp(out[i].data_ptr()), vp(sc[i].data_ptr()), vp(ws[i].data_ptr()),
+                                           nat.stream_ptr()))
+        return float(reduce([x.clone() for x in sc]).cpu().numpy()[0])
+
+    for step in range(nsteps):
+        t = t0 + step * h
+        ap = fh.approx_at(t + 0.5 * h, validate=False)
+        y = [ys[i][own[i]] for i in range(ns)]
+        nrm0 = float(cdot(y, y)[0]) ** 0.5
+        if nrm0 == 0.0:
+            raise ValueError("starting vector must be nonzero")
+        # basis vectors are box-sized (the matvec reads them in place, its exchange fills their
+        # halo planes); u_0 = y itself, s_0 = 1 / ||y|| (the final combine is elementwise, so it
+        # may overwrite y in place)
+        UB = [list(ys)]
+        U = [[UB[0][i][own[i]] for i in range(ns)]]
+        s = [1.0 / nrm0]
+        alpha, beta = [], []
+        for k in range(m):
+            w = matvec(ap, UB[k])
+            alpha.append(s[k] * s[k] * float(cdot(U[k], w)[0]))  # alpha_k = s_k^2 u_k^H A u_k
+            if k == m - 1:
+                break
+            nb = [torch.empty_like(x) for x in ys]
+            nxt = [nb[i][own[i]] for i in range(ns)]
+            cp = -beta[k - 1] * s[k - 1] if k > 0 else 0.0
+            bk = update(s[k], w, -alpha[k] * s[k], U[k], cp, U[k - 1] if k > 0 else None, nxt) ** 0.5
+            if bk <= _BREAKDOWN_TOL:
+                break
+            beta.append(bk)
+            UB.append(nb)
+            U.append(nxt)
+            s.append(1.0 / bk)
+        mm = len(alpha)
+        col = expm_tridiag_column(np.array(alpha), np.array(beta[:mm - 1]), h)
+        # y = ||y|| sum_k col_k v_k = ||y|| sum_k col_k s_k u_k
+        coef = np.empty(2 * mm)
+        for k in range(mm):
+            ck = complex(col[k]) * s[k] * nrm0
+            coef[2 * k], coef[2 * k + 1] = ck.real, ck.imag
+        for i in range(ns):
+            ptrs = (ctypes.c_void_p * mm)(*[U[k][i].data_ptr() for k in range(mm)])
+            nat.check(L.hp_lincomb(nloc[i], mm, ctypes.cast(ptrs, ctypes.c_void_p),
+                                   coef.ctypes.data_as(ctypes.c_void_p), vp(y[i].data_ptr()), nat.stream_ptr()))
+    return ys

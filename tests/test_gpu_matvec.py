@@ -603,3 +603,28 @@ def test_alternate_single_pass_kernels(env):
                          capture_output=True, text=True, timeout=600, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) < TOL
+
+
+def test_device_entry_points_bounded_memory(hp):
+    """A stepping loop hands apply_into / apply_host_into a new surrogate object every step
+    (time-dependent W): device memory must not grow with the number of steps (the term-array
+    cache is a small LRU, the workspace and staging buffers are shared)."""
+    import torch
+
+    w = W.CONFIGS["cfg4"].scaled(20, "cfg4m")
+    s = hp.build_full(w.dim, w.bound)
+    appl = hp.get_applier(s)
+    x = torch.from_numpy(W.coefficients(w)).cuda()
+    y = torch.empty_like(x)
+    xh, yh = x.cpu().pin_memory(), torch.empty(x.shape, dtype=x.dtype).pin_memory()
+    for k in range(3):
+        appl.apply_into(w.approx(0.01 * k), x, y)
+        appl.apply_host_into(w.approx(0.01 * k), xh, yh)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    for k in range(3, 60):
+        appl.apply_into(w.approx(0.01 * k), x, y)
+        appl.apply_host_into(w.approx(0.01 * k), xh, yh)
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() - base < (1 << 20)
+    assert torch.allclose(yh.cuda(), y, rtol=0, atol=0) or rel_l2(yh.numpy(), y.cpu().numpy()) < TOL

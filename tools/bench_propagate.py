@@ -1,6 +1,7 @@
 """Time the propagation runs of BASELINE.json on the device (and the oracle on a sample of steps).
 
     python tools/bench_propagate.py cfg1 [--steps N] [--cpu-steps M]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/bench_propagate.py cfg4   (slab-sharded)
 
 Prints one JSON line: device ms/step (CUDA events around whole steps, state
 resident on the device, term lists re-interpolated on the host each step as
@@ -19,7 +20,68 @@ import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
+def sharded_main(args, rank, world, local_rank):
+    """torchrun --nproc-per-node N tools/bench_propagate.py cfg4: slab-sharded Magnus steps
+    (sharding.sharded_propagate, halos and reductions over NCCL), device time max over ranks."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1403_3511_b200 as hp
+    from paper_1403_3511_b200 import workloads as W
+    from paper_1403_3511_b200.sharding import SlabShard, sharded_propagate
+
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    w = W.CONFIGS[args.workload]
+    if w.kind != "full" or w.batch != 1:
+        raise SystemExit("sharded propagation: full-cube single-vector workloads (cfg4)")
+    nsteps = args.steps or w.nsteps
+    shard = SlabShard(w.dim, w.bound, rank, world, halo=w.degree)
+    g = shard.geo
+    y = torch.zeros(g.box_size, dtype=torch.complex128, device="cuda")
+    y[g.own_slice] = torch.from_numpy(shard.local_coefficients(W, w)[g.own_slice]).cuda()
+    fh = hp.FastHamiltonian(hp.build_full(w.dim, w.bound), hp.custom_potential(w.evaluator, w.dim, W.HALFWIDTH),
+                            w.degree)
+    sharded_propagate([shard], fh, [y.clone()], 0.0, w.dt, 1, args.m)  # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sharded_propagate([shard], fh, [y], 0.0, w.dt, nsteps, args.m)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / nsteps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    nrm = torch.linalg.vector_norm(y[g.own_slice]).square().reshape(1)
+    from paper_1403_3511_b200.sharding import fixed_order_sum
+
+    nrm = float(fixed_order_sum(nrm)[0]) ** 0.5
+    if rank == 0:
+        n = g.global_size
+        out = {"workload": w.name, "n": n, "steps": nsteps, "dt": w.dt, "m": args.m, "n_gpus": world,
+               "parallelism": f"slab-j1 x{world}", "device_ms_per_step": round(float(t), 4),
+               "algorithmic_bytes_per_step": (112 * args.m - 48) * n, "state_norm": nrm}
+        out["achieved_GBs"] = round(out["algorithmic_bytes_per_step"] / (float(t) * 1e-3) / 1e9, 1)
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
+    import os
+
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or "--shard" in sys.argv:
+        ap = argparse.ArgumentParser()
+        ap.add_argument("workload")
+        ap.add_argument("--steps", type=int, default=None)
+        ap.add_argument("--cpu-steps", type=int, default=0)
+        ap.add_argument("--m", type=int, default=7)
+        ap.add_argument("--shard", action="store_true", help="sharded code path even at one rank (torchrun)")
+        args = ap.parse_args()
+        sharded_main(args, int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ.get("LOCAL_RANK", 0)))
+        return
     ap = argparse.ArgumentParser()
     ap.add_argument("workload")
     ap.add_argument("--steps", type=int, default=None)
