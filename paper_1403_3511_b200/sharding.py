@@ -197,111 +197,157 @@ def local_sum(partials):
     return total
 
 
+class DeviceStepOps:
+    """The per-shard kernels of sharded_propagate on the device (the library's entry points).
+
+    Tests substitute an object with the same methods (e.g. numpy + the oracle on CPU under
+    gloo) to check the distributed orchestration on its own."""
+
+    def __init__(self, shards, ys, fh, exchange=None):
+        import torch
+
+        from . import _native as nat
+        from .fast_apply import get_applier
+
+        self.nat, self.L = nat, nat.lib()
+        self.shards, self.fh, self.exchange = shards, fh, exchange
+        self.q = float(fh.potential.harmonic_part)
+        self.appls = [get_applier(sh.set) for sh in shards]
+        self.own = [sh.geo.own_slice for sh in shards]
+        self.nloc = [o.stop - o.start for o in self.own]
+        self.outs = [torch.zeros_like(y) for y in ys]
+        self.ws = [torch.empty(int(self.L.hp_reduce_workspace_bytes(n)), dtype=torch.uint8, device="cuda")
+                   for n in self.nloc]
+
+    def approx(self, t):
+        return self.fh.approx_at(t, validate=False)
+
+    def new_box(self, like):
+        import torch
+
+        return torch.empty_like(like)
+
+    def matvec(self, ap, boxes):
+        """A(t) u on the owned planes of every shard (views into the output boxes); `boxes` are
+        box-sized vectors (owned planes valid) whose halos the exchange fills."""
+        nat = self.nat
+        if self.exchange is None:
+            for i, sh in enumerate(self.shards):
+                sh.apply_polynomial(self.appls[i], ap, boxes[i], self.outs[i], nat.HP_ADD_OSC)
+        else:  # emulated ranks: one exchange over all boxes, then the local matvecs
+            self.exchange([sh.geo for sh in self.shards], boxes)
+            for i in range(len(self.shards)):
+                self.appls[i].apply_into(ap, boxes[i], self.outs[i], nat.HP_ADD_OSC)
+        w = [self.outs[i][self.own[i]] for i in range(len(self.shards))]
+        if self.q != 0.0:
+            for i in range(len(self.shards)):
+                w[i].add_(self.appls[i].apply_square_sum(boxes[i])[self.own[i]], alpha=self.q)
+        return w
+
+    def cdot(self, a, b):
+        """per shard: a^H b as a float64 (re, im) tensor (fixed summation order)"""
+        import ctypes
+
+        import torch
+
+        vp, out = ctypes.c_void_p, []
+        for i in range(len(a)):
+            sc = torch.zeros(2, dtype=torch.float64, device="cuda")
+            self.nat.check(self.L.hp_cdot(self.nloc[i], vp(a[i].data_ptr()), vp(b[i].data_ptr()),
+                                          vp(sc.data_ptr()), vp(self.ws[i].data_ptr()), self.nat.stream_ptr()))
+            out.append(sc)
+        return out
+
+    def update(self, cw, w, cu, u, cp, prev, out):
+        """out = cw w + cu u + cp prev (prev may be None); per shard ||out||^2 as (x, 0)"""
+        import ctypes
+
+        import torch
+
+        vp, parts = ctypes.c_void_p, []
+        for i in range(len(w)):
+            sc = torch.zeros(2, dtype=torch.float64, device="cuda")
+            self.nat.check(self.L.hp_lincomb3_nrm2sq(
+                self.nloc[i], cw, vp(w[i].data_ptr()), cu, vp(u[i].data_ptr()), cp,
+                vp(prev[i].data_ptr()) if prev is not None else None, vp(out[i].data_ptr()), vp(sc.data_ptr()),
+                vp(self.ws[i].data_ptr()), self.nat.stream_ptr()))
+            parts.append(sc)
+        return parts
+
+    def combine(self, U, coef, out):
+        """out = sum_k coef_k U_k per shard (elementwise: out may alias U_0)"""
+        import ctypes
+
+        mm = len(U)
+        c = np.empty(2 * mm)
+        c[0::2], c[1::2] = np.real(coef), np.imag(coef)
+        for i in range(len(out)):
+            ptrs = (ctypes.c_void_p * mm)(*[U[k][i].data_ptr() for k in range(mm)])
+            self.nat.check(self.L.hp_lincomb(self.nloc[i], mm, ctypes.cast(ptrs, ctypes.c_void_p),
+                                             c.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(out[i].data_ptr()),
+                                             self.nat.stream_ptr()))
+
+    def expm_col(self, alpha, beta, h):
+        from .krylov_propagator import expm_tridiag_column
+
+        return expm_tridiag_column(np.array(alpha), np.array(beta), h)
+
+
 def sharded_propagate(shards, fh, ys, t0: float, h: float, nsteps: int, m: int, *, reduce=dist_sum,
-                      exchange=None):
+                      exchange=None, ops=None, breakdown_tol: float = 1e-14):
     """Midpoint Magnus steps (krylov_propagator.py:192-263, lanczos :58-104, expm :173-186) with
     the state split in j1-slabs: SURVEY.md §8(e).
 
     ``shards`` are this process's SlabShard(s) (one per rank; several only when tests emulate
-    the ranks in one process), ``ys`` their box-sized complex128 device states (owned planes
-    valid, halos are refreshed by each matvec's exchange), ``fh`` the FastHamiltonian of the
-    full cube (its surrogate is re-interpolated at every step's midpoint, as the reference
-    does).  Every vector operation runs on the owned planes of each shard; Lanczos dot products
-    and norms are per-shard partials combined by ``reduce`` (all-gather + rank-ordered sum).
+    the ranks in one process), ``ys`` their box-sized complex128 states (owned planes valid,
+    halos are refreshed by each matvec's exchange), ``fh`` the FastHamiltonian of the full cube
+    (its surrogate is re-interpolated at every step's midpoint, as the reference does).  Every
+    vector operation runs on the owned planes of each shard; Lanczos dot products and norms are
+    per-shard partials combined by ``reduce`` (all-gather + rank-ordered sum), so every rank
+    holds identical alpha, beta.
 
-    The basis is kept unnormalised (u_k = v_k / s_k with known s_k), so each Lanczos iteration
-    is the sharded matvec on u_k, one dot (hp_cdot) and one fused update + norm pass
-    (hp_lincomb3_nrm2sq: u_{k+1} = s_k A u_k - alpha_k s_k u_k - beta_{k-1} s_{k-1} u_{k-1});
-    the step ends with one combine pass (hp_lincomb).  Returns ``ys`` advanced in place.
+    The basis is kept unnormalised (u_k = v_k / s_k with known s_k) and box-sized (the matvec
+    reads it in place), so a Lanczos iteration is the sharded matvec on u_k, one dot and one
+    fused update + norm pass (u_{k+1} = s_k A u_k - alpha_k s_k u_k - beta_{k-1} s_{k-1}
+    u_{k-1}); the step ends with one combine pass written over the state.  ``ops`` supplies
+    the per-shard kernels (default DeviceStepOps).  Returns ``ys`` advanced in place.
     """
-    import ctypes
-
-    import torch
-
-    from . import _native as nat
-    from .fast_apply import get_applier
-    from .krylov_propagator import _BREAKDOWN_TOL, expm_tridiag_column
-
-    L = nat.lib()
-    q = float(fh.potential.harmonic_part)
+    ops = ops or DeviceStepOps(shards, ys, fh, exchange)
     ns = len(shards)
-    appls = [get_applier(sh.set) for sh in shards]
     own = [sh.geo.own_slice for sh in shards]
-    nloc = [own[i].stop - own[i].start for i in range(ns)]
-    outs = [torch.zeros_like(y) for y in ys]
-    ws = [torch.empty(int(L.hp_reduce_workspace_bytes(nloc[i])), dtype=torch.uint8, device="cuda")
-          for i in range(ns)]
-    sc = [torch.zeros(2, dtype=torch.float64, device="cuda") for _ in range(ns)]
-    vp = ctypes.c_void_p
 
-    def matvec(ap, boxes):
-        """A(t) u on the owned planes of every shard (views into `outs`); `boxes` are the
-        box-sized basis vectors (owned planes valid), whose halos the exchange fills."""
-        if exchange is None:
-            for i, sh in enumerate(shards):
-                sh.apply_polynomial(appls[i], ap, boxes[i], outs[i], nat.HP_ADD_OSC)
-        else:  # emulated ranks: one exchange over all boxes, then the local matvecs
-            exchange([sh.geo for sh in shards], boxes)
-            for i in range(ns):
-                appls[i].apply_into(ap, boxes[i], outs[i], nat.HP_ADD_OSC)
-        w = [outs[i][own[i]] for i in range(ns)]
-        if q != 0.0:
-            for i in range(ns):
-                w[i].add_(appls[i].apply_square_sum(boxes[i])[own[i]], alpha=q)
-        return w
-
-    def cdot(a, b):  # sum over ranks of a^H b -> (re, im)
-        for i in range(ns):
-            nat.check(L.hp_cdot(nloc[i], vp(a[i].data_ptr()), vp(b[i].data_ptr()), vp(sc[i].data_ptr()),
-                                vp(ws[i].data_ptr()), nat.stream_ptr()))
-        return reduce([x.clone() for x in sc]).cpu().numpy()
-
-    def update(cw, w, cu, u, cp, prev, out):  # out = cw w + cu u + cp prev; returns sum ||out||^2
-        for i in range(ns):
-            nat.check(L.hp_lincomb3_nrm2sq(nloc[i], cw, vp(w[i].data_ptr()), cu, vp(u[i].data_ptr()), cp,
-                                           vp(prev[i].data_ptr()) if prev is not None else None,
-                                           vp(out[i].data_ptr()), vp(sc[i].data_ptr()), vp(ws[i].data_ptr()),
-                                           nat.stream_ptr()))
-        return float(reduce([x.clone() for x in sc]).cpu().numpy()[0])
+    def total(parts):
+        return reduce([p.clone() for p in parts])
 
     for step in range(nsteps):
         t = t0 + step * h
-        ap = fh.approx_at(t + 0.5 * h, validate=False)
+        ap = ops.approx(t + 0.5 * h)
         y = [ys[i][own[i]] for i in range(ns)]
-        nrm0 = float(cdot(y, y)[0]) ** 0.5
+        nrm0 = float(total(ops.cdot(y, y))[0]) ** 0.5
         if nrm0 == 0.0:
             raise ValueError("starting vector must be nonzero")
-        # basis vectors are box-sized (the matvec reads them in place, its exchange fills their
-        # halo planes); u_0 = y itself, s_0 = 1 / ||y|| (the final combine is elementwise, so it
-        # may overwrite y in place)
-        UB = [list(ys)]
-        U = [[UB[0][i][own[i]] for i in range(ns)]]
+        UB = [list(ys)]  # u_0 = y itself, s_0 = 1 / ||y||
+        U = [y]
         s = [1.0 / nrm0]
         alpha, beta = [], []
         for k in range(m):
-            w = matvec(ap, UB[k])
-            alpha.append(s[k] * s[k] * float(cdot(U[k], w)[0]))  # alpha_k = s_k^2 u_k^H A u_k
+            w = ops.matvec(ap, UB[k])
+            alpha.append(s[k] * s[k] * float(total(ops.cdot(U[k], w))[0]))  # s_k^2 u_k^H A u_k
             if k == m - 1:
                 break
-            nb = [torch.empty_like(x) for x in ys]
+            nb = [ops.new_box(x) for x in ys]
             nxt = [nb[i][own[i]] for i in range(ns)]
             cp = -beta[k - 1] * s[k - 1] if k > 0 else 0.0
-            bk = update(s[k], w, -alpha[k] * s[k], U[k], cp, U[k - 1] if k > 0 else None, nxt) ** 0.5
-            if bk <= _BREAKDOWN_TOL:
+            bk = float(total(ops.update(s[k], w, -alpha[k] * s[k], U[k], cp, U[k - 1] if k > 0 else None,
+                                        nxt))[0]) ** 0.5
+            if bk <= breakdown_tol:
                 break
             beta.append(bk)
             UB.append(nb)
             U.append(nxt)
             s.append(1.0 / bk)
         mm = len(alpha)
-        col = expm_tridiag_column(np.array(alpha), np.array(beta[:mm - 1]), h)
+        col = ops.expm_col(alpha, beta[:mm - 1], h)
         # y = ||y|| sum_k col_k v_k = ||y|| sum_k col_k s_k u_k
-        coef = np.empty(2 * mm)
-        for k in range(mm):
-            ck = complex(col[k]) * s[k] * nrm0
-            coef[2 * k], coef[2 * k + 1] = ck.real, ck.imag
-        for i in range(ns):
-            ptrs = (ctypes.c_void_p * mm)(*[U[k][i].data_ptr() for k in range(mm)])
-            nat.check(L.hp_lincomb(nloc[i], mm, ctypes.cast(ptrs, ctypes.c_void_p),
-                                   coef.ctypes.data_as(ctypes.c_void_p), vp(y[i].data_ptr()), nat.stream_ptr()))
+        ops.combine(U[:mm], np.array([complex(col[k]) * s[k] * nrm0 for k in range(mm)]), y)
     return ys
