@@ -21,7 +21,7 @@
 #define Q_CONST 0
 #endif
 #ifndef Q_FENCES
-#define Q_FENCES 1
+#define Q_FENCES 0  // compiler fences between load phases: off measured 0.8% faster (2.416 vs 2.434 ms)
 #endif
 #if Q_FENCES
 #define Q_FENCE() asm volatile("" ::: "memory")
