@@ -209,12 +209,10 @@ class PolynomialApplier:
 
         Reads input planes plane_lo - 4 .. plane_hi + 3 (hp_apply_polynomial_planes).  Returns
         False (nothing launched) when the surrogate is outside the fused full-cube class; the
-        answer is cached per (approx, flags).
+        answer is cached per term structure (degrees and nonzero pattern), shape and flags.
         """
-        import torch
-
         _, degs, coeffs, h, _batch, dtype, ws = self._into_entry(approx, x, flags, 1)
-        key = (id(approx), tuple(x.shape), x.dtype, flags)
+        key = (degs.tobytes(), (np.asarray(coeffs) != 0).tobytes(), tuple(x.shape), x.dtype, flags)
         unsupported = self.__dict__.setdefault("_planes_unsupported", set())
         if key in unsupported:
             return False
