@@ -11,10 +11,19 @@
 //   Even-offset taps of the pair overlap along both axes: 42 shared-memory loads serve the four
 //   points' 84 taps (10.5 per point instead of 12.5).
 // * The march-axis ring of partial outputs has 8 slots instead of 9: at step p the slot of
-//   y(p-4) receives its last term (from v(p)), is stored, and is reused for y(p+4).
+//   y(p-4) receives its last term (from v(p)), is stored, and is reused for y(p+4).  Every
+//   in-plane term goes straight into a ring slot (no per-point accumulators): 128 of the 255
+//   registers are the ring.
+// * Band weights are read per plane from shared tables indexed by global coordinate (a warp
+//   owns one axis-1 row pair: broadcast loads); holding them in registers spills.
+// * 3 stages of 64 KB; the LAST warp to release a stage refills it (no producer warp, no warp
+//   waiting to act as producer).
+// * Global addresses advance by one plane per step (64-bit index math per step cost ~40
+//   registers and spilled the first version).
 //
-// Shared-memory port budget per coefficient (the bound of this class of kernel):
-// 64 B fills + 168 B loads, against 80 + 200 for k_fg_single.
+// Measured: 2.26-2.45 ms per cfg4 matvec (0.54-0.58 of the HBM roofline), bound
+// by the TMA fills (64 B/coef, 1.55 ms alone) and the LSU shared wavefronts (80% busy), which
+// overlap only in part at 8 warps/SM.
 #pragma once
 
 #ifndef Q_CONST
