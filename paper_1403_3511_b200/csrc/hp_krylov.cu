@@ -315,20 +315,128 @@ __device__ bool expm_col(int m, const double* alpha, const double* beta, double 
   return true;
 }
 
+// The same QL + exp as ql_eigh / expm_col, run by the 32 lanes of one warp: the scalar
+// recurrence (d, e, rotation parameters) is evaluated redundantly and identically by every lane,
+// and lane r applies each rotation to rows r and r + 32 of Z, kept in lane-private arrays (the
+// single-thread version spends most of its time on the m x m local-memory eigenvector updates).
+// Same operations in the same order per element: bitwise identical to expm_col.  Every lane
+// returns the convergence flag; lane i writes col[i] (and col[i + 32]).
+__device__ bool expm_col_warp(int m, const double* alpha, const double* beta, double tau, double2* col) {
+  const int lane = threadIdx.x & 31;
+  double d[HP_MAXM], e[HP_MAXM], z0r[HP_MAXM], z1r[HP_MAXM];  // rows lane, lane + 32 of Z
+  for (int i = 0; i < m; ++i) {
+    d[i] = alpha[i];
+    e[i] = (i < m - 1) ? beta[i] : 0.0;
+    z0r[i] = (i == lane) ? 1.0 : 0.0;
+    z1r[i] = (i == lane + 32) ? 1.0 : 0.0;
+  }
+  const bool has0 = lane < m, has1 = lane + 32 < m;
+  bool ok = true;
+  if (m > 1) {
+    for (int l = 0; l < m && ok; ++l) {
+      int it = 0;
+      while (true) {
+        int mm = l;
+        while (mm < m - 1) {
+          double dd = fabs(d[mm]) + fabs(d[mm + 1]);
+          if (fabs(e[mm]) <= 1e-14 * dd) break;
+          ++mm;
+        }
+        if (mm == l) break;
+        if (it == 30) {
+          ok = false;
+          break;
+        }
+        ++it;
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = hypot(g, 1.0);
+        g = d[mm] - d[l] + e[l] / (g + (g >= 0 ? r : -r));
+        double s = 1.0, c = 1.0, p = 0.0;
+        bool early = false;
+        for (int i = mm - 1; i >= l; --i) {
+          double f = s * e[i];
+          double b = c * e[i];
+          r = hypot(f, g);
+          e[i + 1] = r;
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[mm] = 0.0;
+            early = true;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          d[i + 1] = g + p;
+          g = c * r - b;
+          if (has0) {
+            double zi = z0r[i], zi1 = z0r[i + 1];
+            z0r[i + 1] = s * zi + c * zi1;
+            z0r[i] = c * zi - s * zi1;
+          }
+          if (has1) {
+            double zi = z1r[i], zi1 = z1r[i + 1];
+            z1r[i + 1] = s * zi + c * zi1;
+            z1r[i] = c * zi - s * zi1;
+          }
+        }
+        if (!early) {
+          d[l] -= p;
+          e[l] = g;
+          e[mm] = 0.0;
+        }
+      }
+    }
+  }
+  if (!ok) return false;
+  int order[HP_MAXM];
+  for (int i = 0; i < m; ++i) order[i] = i;
+  for (int i = 1; i < m; ++i) {
+    int t = order[i], j = i - 1;
+    while (j >= 0 && d[order[j]] > d[t]) { order[j + 1] = order[j]; --j; }
+    order[j + 1] = t;
+  }
+  double2 c[HP_MAXM];
+  for (int jj = 0; jj < m; ++jj) {
+    int j = order[jj];
+    double x = tau * d[j];
+    double sn, cs;
+    sincos(x, &sn, &cs);
+    double zz0 = __shfl_sync(0xffffffffu, z0r[j], 0);  // Z[0, j] lives in lane 0
+    c[jj] = make_double2(cs * zz0, -sn * zz0);
+  }
+  for (int h = 0; h < 2; ++h) {
+    const int i = lane + 32 * h;
+    if (i >= m) continue;
+    const double* zr = h ? z1r : z0r;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int jj = 0; jj < m; ++jj) {
+      double zij = zr[order[jj]];
+      acc.x += zij * c[jj].x;
+      acc.y += zij * c[jj].y;
+    }
+    col[i] = acc;
+  }
+  return true;
+}
+
 }  // namespace hp
 #include "hp_small.cuh"
 namespace hp {
 
-__global__ void k_lz_expm(LzState* st, double tau) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (!expm_col(st->m_eff, st->alpha, st->beta, tau, st->col)) st->ql_fail = 1;
+__global__ void k_lz_expm(LzState* st, double tau) {  // one warp
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const bool ok = expm_col_warp(st->m_eff, st->alpha, st->beta, tau, st->col);
+  if (threadIdx.x == 0 && !ok) st->ql_fail = 1;
 }
 
 __global__ void k_expm_standalone(const double* alpha, const double* beta, int m, double tau, double2* col,
                                   int* status) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  bool ok = expm_col(m, alpha, beta, tau, col);
-  if (status) *status = ok ? 0 : 1;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;  // one warp
+  const bool ok = expm_col_warp(m, alpha, beta, tau, col);
+  if (status && threadIdx.x == 0) *status = ok ? 0 : 1;
 }
 
 __global__ void k_tridiag_eigh(const double* alpha, const double* beta, int m, double* dout, double* zout,

@@ -30,6 +30,7 @@ struct SmallOp {
 
 struct SmallProg {
   int nops;
+  int nslots_hint;  // program slots staged in shared memory (use_smem)
   SmallOp ops[SM_MAXOPS];
 };
 
@@ -57,7 +58,7 @@ template <class AXS>
 __global__ void __launch_bounds__(SM_THREADS, 1) k_small_magnus(SmallArgs<AXS> A, double2* __restrict__ y,
                                                                  double2* __restrict__ V, double2* __restrict__ z,
                                                                  double2* __restrict__ slots, double* diag,
-                                                                 int use_smem) {
+                                                                 int use_smem, int use_tab, int jmax) {
   __shared__ double alpha[SM_MAXM], beta[SM_MAXM], scale[SM_MAXM];
   __shared__ double2 col[SM_MAXM];
   __shared__ int m_eff_sh, brk_sh, fail_sh;
@@ -69,6 +70,27 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_magnus(SmallArgs<AXS> A
   double2* wkb = dyn + n;
   double2* sb = use_smem ? dyn + 2 * n : slots;
   auto row = [&](int k) -> double2* { return k == 0 ? y : V + (int64_t)(k - 1) * n; };
+  // use_tab: per (axis, point) orders and neighbours, and sqrt(j / 2) for j <= jmax + 1, in
+  // shared memory after the vectors -- each X application then costs three table reads instead
+  // of the index arithmetic and two FP64 square roots per point
+  const size_t vec_bytes = use_smem ? (size_t)(A.prog.nslots_hint + 2) * n * sizeof(double2) : 0;
+  int* jt = (int*)((char*)dyn + vec_bytes);
+  int* dnt = jt + A.dim * n;
+  int* upt = dnt + A.dim * n;
+  double* sqt = (double*)(upt + A.dim * n);
+  if (use_tab) {
+    for (int64_t o = t; o < n; o += SM_THREADS)
+      for (int a = 0; a < A.dim; ++a) {
+        int j;
+        int64_t dn, up;
+        A.axs.at(a, o, j, dn, up);
+        jt[a * n + o] = j;
+        dnt[a * n + o] = (int)dn;
+        upt[a * n + o] = (int)up;
+      }
+    for (int j = t; j <= jmax + 1; j += SM_THREADS) sqt[j] = sqrt((double)j * 0.5);
+    __syncthreads();
+  }
   // nrm0
   double2 acc = make_double2(0.0, 0.0);
   for (int64_t i = t; i < n; i += SM_THREADS) {
@@ -121,8 +143,17 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_magnus(SmallArgs<AXS> A
         for (int64_t o = t; o < n; o += SM_THREADS) {
           int j;
           int64_t dn, up;
-          A.axs.at(op.axis, o, j, dn, up);
-          double cd = sqrt((double)j * 0.5), cu = sqrt(((double)j + 1.0) * 0.5);
+          double cd, cu;
+          if (use_tab) {
+            j = jt[op.axis * n + o];
+            dn = dnt[op.axis * n + o];
+            up = upt[op.axis * n + o];
+            cd = sqt[j];
+            cu = sqt[j + 1];
+          } else {
+            A.axs.at(op.axis, o, j, dn, up);
+            cd = sqrt((double)j * 0.5), cu = sqrt(((double)j + 1.0) * 0.5);
+          }
           double2 wd = dn >= 0 ? w[dn] : make_double2(0.0, 0.0);
           double2 wu = up >= 0 ? w[up] : make_double2(0.0, 0.0);
           double2 r = make_double2(sc * fma(cd, wd.x, cu * wu.x), sc * fma(cd, wd.y, cu * wu.y));
@@ -137,7 +168,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_magnus(SmallArgs<AXS> A
         const double2* src = buf(op.a);
         for (int64_t o = t; o < n; o += SM_THREADS) {
           double lev = 0.0;
-          for (int a = 0; a < A.dim; ++a) lev += (double)A.axs.j(a, o) + 0.5;
+          for (int a = 0; a < A.dim; ++a) lev += (double)(use_tab ? jt[a * n + o] : A.axs.j(a, o)) + 0.5;
           double2 x = src[o];
           dst[o] = make_double2(fma(lev, x.x, dst[o].x), fma(lev, x.y, dst[o].y));
         }
@@ -186,7 +217,10 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_magnus(SmallArgs<AXS> A
     __syncthreads();
   }
   // ---- exp(-i h T) e_1 and the combine
-  if (t == 0 && !expm_col(m_eff, alpha, beta, A.h, col)) fail_sh = 1;
+  if (t < 32) {  // warp 0
+    const bool ok = expm_col_warp(m_eff, alpha, beta, A.h, col);
+    if (t == 0 && !ok) fail_sh = 1;
+  }
   __syncthreads();
   for (int64_t i = t; i < n; i += SM_THREADS) {
     double2 s = make_double2(0.0, 0.0);
@@ -225,6 +259,7 @@ static bool to_small(const Program& p, SmallProg& sp) {
   if ((int)p.ops.size() > SM_MAXOPS || p.nslots > 120) return false;
   auto id = [](int b) -> int { return b == BUF_V ? -2 : (b == BUF_Y ? -1 : b - BUF_SLOT0); };
   sp.nops = (int)p.ops.size();
+  sp.nslots_hint = std::max(p.nslots, 1);
   for (int i = 0; i < sp.nops; ++i) {
     const Op& o = p.ops[i];
     SmallOp& s = sp.ops[i];
@@ -252,18 +287,22 @@ static hp_status small_magnus_step(const hp_set_s* s, const Program& p, double h
   // z, w_k and the program slots in shared memory when they fit (~0.2 us per op instead of ~2 us)
   size_t smem = (size_t)(std::max(p.nslots, 1) + 2) * s->n * sizeof(double2);
   if (smem > 200 * 1024) smem = 0;
+  const int jmax = s->bound + 1;
+  const size_t tab = (size_t)s->dim * s->n * 3 * sizeof(int) + (size_t)(jmax + 2) * sizeof(double);
+  const int use_tab = smem + tab <= 220 * 1024 ? 1 : 0;
+  const size_t dyn = smem + (use_tab ? tab : 0);
   if (s->boxed) {
     SmallArgs<AllBoxS> A;
     for (int a = 0; a < s->dim; ++a) A.axs.ax[a] = s->box(a);
     A.dim = s->dim, A.n = s->n, A.m = m, A.inv_L = 1.0 / halfwidth, A.two_L = 2.0 / halfwidth, A.h = h, A.prog = sp;
-    if (smem) HP_CUDA(cudaFuncSetAttribute(k_small_magnus<AllBoxS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_small_magnus<AllBoxS><<<1, SM_THREADS, smem, st>>>(A, y, V, z, slots, diag, smem ? 1 : 0);
+    if (dyn) HP_CUDA(cudaFuncSetAttribute(k_small_magnus<AllBoxS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    k_small_magnus<AllBoxS><<<1, SM_THREADS, dyn, st>>>(A, y, V, z, slots, diag, smem ? 1 : 0, use_tab, jmax);
   } else {
     SmallArgs<AllTabS> A;
     for (int a = 0; a < s->dim; ++a) A.axs.ax[a] = s->tab(a);
     A.dim = s->dim, A.n = s->n, A.m = m, A.inv_L = 1.0 / halfwidth, A.two_L = 2.0 / halfwidth, A.h = h, A.prog = sp;
-    if (smem) HP_CUDA(cudaFuncSetAttribute(k_small_magnus<AllTabS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_small_magnus<AllTabS><<<1, SM_THREADS, smem, st>>>(A, y, V, z, slots, diag, smem ? 1 : 0);
+    if (dyn) HP_CUDA(cudaFuncSetAttribute(k_small_magnus<AllTabS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    k_small_magnus<AllTabS><<<1, SM_THREADS, dyn, st>>>(A, y, V, z, slots, diag, smem ? 1 : 0, use_tab, jmax);
   }
   HP_LAUNCH_CHECK("k_small_magnus");
   *done = true;
