@@ -57,8 +57,9 @@ class ClockSampler:
     # NVML clocks-event reason bits
     BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, interval: float = 0.002):
         self.index = index
+        self.interval = interval
         self.proc = None
         self.lines: list[str] = []
         self.samples: list[tuple[float, float, int]] = []
@@ -104,9 +105,8 @@ class ClockSampler:
             pass
 
     def _poll(self):
-        while not self.stop.is_set():
+        while not self.stop.wait(self.interval):
             self._sample()
-            time.sleep(0.002)
 
     def _read(self):
         for line in self.proc.stdout:
