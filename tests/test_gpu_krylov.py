@@ -152,3 +152,35 @@ def test_sharded_propagation_emulated(bound, world):
     sharded_propagate(shards, fh, ys, 0.0, w.dt, 3, 7, reduce=local_sum, exchange=emulate_exchange)
     got = torch.cat([y[s.geo.own_slice] for s, y in zip(shards, ys)])
     assert float(torch.linalg.vector_norm(got - want) / torch.linalg.vector_norm(want)) < 1e-12
+
+
+def test_lincomb_entry_points():
+    """hp_lincomb3_nrm2sq / hp_lincomb (the sharded Lanczos update and combine) against numpy."""
+    import ctypes
+
+    import torch
+
+    from paper_1403_3511_b200 import _native as nat
+
+    L = nat.lib()
+    gen = np.random.default_rng(3)
+    n = 100_003
+    X, Y, Z = (torch.from_numpy(gen.standard_normal(n) + 1j * gen.standard_normal(n)).cuda() for _ in range(3))
+    out = torch.empty_like(X)
+    nrm = torch.zeros(2, dtype=torch.float64, device="cuda")
+    ws = torch.empty(int(L.hp_reduce_workspace_bytes(n)), dtype=torch.uint8, device="cuda")
+    vp = ctypes.c_void_p
+    for zptr, c in ((Z, -0.25), (None, 0.0)):
+        nat.check(L.hp_lincomb3_nrm2sq(n, 1.5, vp(X.data_ptr()), -0.75, vp(Y.data_ptr()), c,
+                                       vp(zptr.data_ptr()) if zptr is not None else None, vp(out.data_ptr()),
+                                       vp(nrm.data_ptr()), vp(ws.data_ptr()), nat.stream_ptr()))
+        want = 1.5 * X.cpu().numpy() - 0.75 * Y.cpu().numpy() + (c * Z.cpu().numpy() if zptr is not None else 0)
+        assert rel_l2(out.cpu().numpy(), want) < 1e-15
+        assert abs(float(nrm[0]) - np.vdot(want, want).real) <= 1e-13 * np.vdot(want, want).real
+    coef = np.array([0.5, -1.0, 2.0, 0.25, -0.125, 3.0])  # 3 complex coefficients
+    ptrs = (ctypes.c_void_p * 3)(X.data_ptr(), Y.data_ptr(), Z.data_ptr())
+    nat.check(L.hp_lincomb(n, 3, ctypes.cast(ptrs, ctypes.c_void_p), coef.ctypes.data_as(ctypes.c_void_p),
+                           vp(out.data_ptr()), nat.stream_ptr()))
+    cs = coef[0::2] + 1j * coef[1::2]
+    want = cs[0] * X.cpu().numpy() + cs[1] * Y.cpu().numpy() + cs[2] * Z.cpu().numpy()
+    assert rel_l2(out.cpu().numpy(), want) < 1e-15
