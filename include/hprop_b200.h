@@ -149,6 +149,14 @@ hp_status hp_apply_polynomial_planes(hp_set_t s, const int32_t* degrees_host, co
                                      int nterms, double halfwidth, int dtype, const void* in_dev,
                                      void* out_dev, int plane_lo, int plane_hi, int flags,
                                      void* workspace_dev, size_t workspace_bytes, void* stream);
+/* The same, and dot_dev[0..1] += sum over the output planes [plane_lo, plane_hi) of the rows of
+   v^H A v formed inside the kernel (A symmetric: conj(v_p) . row p split at plane p, no second
+   read of v).  Summed over the ranks of a slab decomposition (each owning its planes) it is the
+   global v^H A v: the Lanczos alpha of sharded_propagate (krylov_propagator.py:81). */
+hp_status hp_apply_polynomial_planes_dot(hp_set_t s, const int32_t* degrees_host, const double* coeffs_host,
+                                         int nterms, double halfwidth, int dtype, const void* in_dev,
+                                         void* out_dev, int plane_lo, int plane_hi, int flags, double* dot_dev,
+                                         void* workspace_dev, size_t workspace_bytes, void* stream);
 
 /* apply_square_sum -- fast_apply.py:202-245 (exact restricted sum_l x_l^2) */
 hp_status hp_square_sum(hp_set_t s, int dtype, const void* in_dev, void* out_dev,

@@ -58,6 +58,8 @@ SIGNATURES = {
                                              c_i64, c_int, c_vp, c_sz, c_vp]),
     "hp_apply_polynomial_planes": (c_int, [c_vp, c_i32p, c_dblp, c_int, c_dbl, c_int, c_vp, c_vp, c_int, c_int,
                                            c_int, c_vp, c_sz, c_vp]),
+    "hp_apply_polynomial_planes_dot": (c_int, [c_vp, c_i32p, c_dblp, c_int, c_dbl, c_int, c_vp, c_vp, c_int, c_int,
+                                               c_int, c_vp, c_vp, c_sz, c_vp]),
     "hp_square_sum": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_vp]),
     "hp_magnus_workspace_bytes": (c_sz, [c_vp, c_int, c_i32p, c_int, c_i32p, c_int, c_int]),
     "hp_magnus_step": (c_int, [c_vp, c_int, c_i32p, c_dblp, c_int, c_i32p, c_dblp, c_int, c_dbl, c_dbl,

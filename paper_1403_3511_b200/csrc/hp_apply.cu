@@ -715,9 +715,10 @@ hp_status hp_apply_polynomial_streamed(hp_set_t s, const int32_t* degrees, const
   return HP_OK;
 }
 
-hp_status hp_apply_polynomial_planes(hp_set_t s, const int32_t* degrees, const double* coeffs, int nterms,
-                                     double halfwidth, int dtype, const void* in, void* out, int plane_lo,
-                                     int plane_hi, int flags, void* ws, size_t ws_bytes, void* stream) {
+hp_status hp_apply_polynomial_planes_dot(hp_set_t s, const int32_t* degrees, const double* coeffs, int nterms,
+                                         double halfwidth, int dtype, const void* in, void* out, int plane_lo,
+                                         int plane_hi, int flags, double* dot_dev, void* ws, size_t ws_bytes,
+                                         void* stream) {
   hp_status rc = check_set(s);
   if (rc) return rc;
   if ((rc = check_terms(s, degrees, nterms, halfwidth))) return rc;
@@ -726,13 +727,21 @@ hp_status hp_apply_polynomial_planes(hp_set_t s, const int32_t* degrees, const d
   if (s->n == 0) return HP_OK;
   if (flags & (HP_REF_ORDER | HP_CHECK_FINITE))
     return fail(HP_ERR_VALUE, "plane-range matvec: the fused full-cube evaluator only");
+  if (dot_dev && dtype != HP_C128) return fail(HP_ERR_VALUE, "plane-range dot: complex128 only");
   auto terms = make_terms(s->dim, degrees, coeffs, nterms);
   bool done = false;
   rc = fullgrid_apply_planes(s, terms, halfwidth, dtype, in, out, plane_lo, plane_hi, flags, ws, ws_bytes,
-                             as_stream(stream), &done);
+                             as_stream(stream), &done, dot_dev);
   if (rc) return rc;
   if (!done) return fail(HP_ERR_VALUE, "plane-range matvec: the fused full-cube evaluator only");
   return HP_OK;
+}
+
+hp_status hp_apply_polynomial_planes(hp_set_t s, const int32_t* degrees, const double* coeffs, int nterms,
+                                     double halfwidth, int dtype, const void* in, void* out, int plane_lo,
+                                     int plane_hi, int flags, void* ws, size_t ws_bytes, void* stream) {
+  return hp_apply_polynomial_planes_dot(s, degrees, coeffs, nterms, halfwidth, dtype, in, out, plane_lo, plane_hi,
+                                        flags, nullptr, ws, ws_bytes, stream);
 }
 
 hp_status hp_square_sum(hp_set_t s, int dtype, const void* in, void* out, int64_t batch, void* stream) {

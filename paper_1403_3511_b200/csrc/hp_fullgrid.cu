@@ -42,6 +42,8 @@ constexpr int FG_W = 2 * FG_K + 1;
 constexpr int FG_C = 4;  // inner chunk of pass A (4 x 16 B = 64 B per row segment)
 constexpr int FG_D = 4;  // cp.async prefetch distance (planes)
 constexpr int FG_MAXN = 256;
+constexpr int FG_DOTP = 512;  // per-CTA dot partials (grid <= SM count) at the end of the workspace
+constexpr size_t FG_DOTP_BYTES = FG_DOTP * 16;
 
 // ---------------------------------------------------------------- host tables
 
@@ -106,14 +108,15 @@ struct FgPlan {
   int rm = 0;
   unsigned mask[4] = {0, 0, 0, 0}; // nonzero diagonals of the combined single-axis bands
   unsigned maskG = 0;              // nonzero diagonals of the mixed-term axis-2 bands G_m
+  bool twopass = true;             // the cube fits the two-pass kernels' chunking (single pass: any side)
 };
 
 static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch, int flags) {
   FgPlan P;
   if (!s->boxed || s->dim != 4 || dtype != HP_C128 || batch < 1) return P;
   for (int a = 0; a < 4; ++a) if (s->side[a] > FG_MAXN) return P;
-  if (((int64_t)s->side[2] * s->side[3]) % FG_C != 0) return P;
-  if (s->side[1] * FG_C > 512 || s->side[3] > 128) return P;
+  if (((int64_t)s->side[2] * s->side[3]) % FG_C != 0 || s->side[1] * FG_C > 512 || s->side[3] > 128)
+    P.twopass = false;
   for (const Term& t : terms) {
     int act[4], na = 0;
     for (int a = 0; a < 4; ++a) if (t.r[a] > 0) act[na++] = a;
@@ -478,7 +481,8 @@ size_t fullgrid_workspace_bytes(const hp_set_s* s, const std::vector<Term>& term
                                 int flags) {
   FgPlan F = classify(s, terms, dtype, batch, flags);
   if (!F.ok) return 0;
-  return (size_t)(4 + 2) * FG_MAXN * FG_W * sizeof(double) + 256 + (size_t)s->n * sizeof(double2);
+  // bands | u (two-pass kernels) | per-CTA dot partials of the plane-range entry point
+  return (size_t)(4 + 2) * FG_MAXN * FG_W * sizeof(double) + 256 + (size_t)s->n * sizeof(double2) + FG_DOTP_BYTES;
 }
 
 // classification + band tables; *ok = false when the fused evaluator does not cover the call
@@ -550,7 +554,8 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
       return HP_OK;
     }
   }
-  if (batch != 1) return HP_OK;  // the two-pass kernels take one vector: level evaluator
+  // the two-pass kernels take one vector and need their chunking: otherwise the level evaluator
+  if (batch != 1 || !F.twopass) return HP_OK;
   // pass B
   rc = even ? launch_inner<FG_MASK_EVEN, FG_MASK_EVEN>(s, v, u, P, st)
             : launch_inner<FG_MASK_ALL, FG_MASK_ALL>(s, v, u, P, st);
@@ -579,9 +584,32 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
 
 // y on output j1-planes [plo, phi) only (reads input planes [plo - 4, phi + 4)); *done = false
 // when the set / terms are outside the single-pass class
+// dot_accum[0..1] += sum of the per-CTA partials, in CTA order (one block)
+__global__ void k_fg_dot_accum(const double2* __restrict__ partial, int n, double* __restrict__ acc) {
+  __shared__ double2 sh[256];
+  double2 a = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    a.x += partial[i].x;
+    a.y += partial[i].y;
+  }
+  sh[threadIdx.x] = a;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      sh[threadIdx.x].x += sh[threadIdx.x + w].x;
+      sh[threadIdx.x].y += sh[threadIdx.x + w].y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    acc[0] += sh[0].x;
+    acc[1] += sh[0].y;
+  }
+}
+
 hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                                 const void* in, void* out, int plo, int phi, int flags, void* ws, size_t ws_bytes,
-                                cudaStream_t st, bool* done) {
+                                cudaStream_t st, bool* done, double* dot_accum) {
   *done = false;
   FgPlan F = classify(s, terms, dtype, 1, flags);
   if (!F.ok || !fg_single_class(F)) return HP_OK;
@@ -595,9 +623,20 @@ hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& term
   const double* P = (const double*)ws;
   const double* G = P + 4 * FG_MAXN * FG_W;
   bool launched = false;
-  rc = F.nmix ? launch_single<1>(s, (const double2*)in, (double2*)out, P, G, F, st, nullptr, &launched, plo, phi)
-              : launch_single<0>(s, (const double2*)in, (double2*)out, P, G, F, st, nullptr, &launched, plo, phi);
+  DotOut d;
+  if (dot_accum) {
+    d.partial = (double2*)((char*)ws + fullgrid_workspace_bytes(s, terms, dtype, 1, flags) - FG_DOTP_BYTES);
+    d.capacity = FG_DOTP;
+  }
+  DotOut* dp = dot_accum ? &d : nullptr;
+  rc = F.nmix ? launch_single<1>(s, (const double2*)in, (double2*)out, P, G, F, st, dp, &launched, plo, phi)
+              : launch_single<0>(s, (const double2*)in, (double2*)out, P, G, F, st, dp, &launched, plo, phi);
   if (rc) return rc;
+  if (launched && dot_accum) {
+    if (d.n == 0) return fail(HP_ERR_RUNTIME, "plane-range matvec: fused dot unavailable");
+    k_fg_dot_accum<<<1, 256, 0, st>>>(d.partial, d.n, dot_accum);
+    HP_LAUNCH_CHECK("k_fg_dot_accum");
+  }
   *done = launched;
   return HP_OK;
 }

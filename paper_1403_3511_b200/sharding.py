@@ -147,34 +147,39 @@ class SlabShard:
         ihi = hi - (RADIUS if g.rank < g.world - 1 else 0)
         return (ilo, ihi) if ihi > ilo else None
 
-    def apply_polynomial(self, appl, ap, x, y, flags: int = 0, overlap: bool = True, exchange=None):
+    def apply_polynomial(self, appl, ap, x, y, flags: int = 0, overlap: bool = True, exchange=None, dot=None):
         """y[own] = W(X) x on this rank's planes; x, y are box-sized device tensors.
 
         With `overlap`, the halo exchange runs on a side stream while the interior planes are
         computed (hp_apply_polynomial_planes), then the boundary planes; otherwise exchange,
         then one matvec over the box.  `exchange(geo, x)` replaces halo_exchange (tests).
+        `dot` (a float64 device tensor of 2): the owned rows of x^H y are added to it by the
+        fused kernel when the surrogate is in its class; returns whether it was.
         """
         import torch
 
         exch = exchange or halo_exchange
-        rng = self.interior() if overlap and self.geo.world > 1 else None
-        if rng is None or not appl.apply_planes_into(ap, x, y, rng[0], rng[0], flags):
-            exch(self.geo, x)
-            appl.apply_into(ap, x, y, flags)
-            return
         g = self.geo
         lo, hi = g.lo - g.blo, g.hi - g.blo
+        rng = self.interior() if overlap and g.world > 1 else None
+        if rng is None or not appl.apply_planes_into(ap, x, y, rng[0], rng[0], flags):
+            exch(g, x)
+            if dot is not None and appl.apply_planes_into(ap, x, y, lo, hi, flags, dot=dot):
+                return True
+            appl.apply_into(ap, x, y, flags)
+            return False
         main = torch.cuda.current_stream()
         side = self.__dict__.setdefault("_side", torch.cuda.Stream())
         side.wait_stream(main)
         with torch.cuda.stream(side):
             exch(g, x)  # NCCL on the side stream
-        appl.apply_planes_into(ap, x, y, rng[0], rng[1], flags)  # reads owned planes only
+        appl.apply_planes_into(ap, x, y, rng[0], rng[1], flags, dot=dot)  # reads owned planes only
         main.wait_stream(side)
         if rng[0] > lo:
-            appl.apply_planes_into(ap, x, y, lo, rng[0], flags)
+            appl.apply_planes_into(ap, x, y, lo, rng[0], flags, dot=dot)
         if hi > rng[1]:
-            appl.apply_planes_into(ap, x, y, rng[1], hi, flags)
+            appl.apply_planes_into(ap, x, y, rng[1], hi, flags, dot=dot)
+        return dot is not None
 
 
 # ---------------------------------------------------------------- sharded time stepping
@@ -229,20 +234,33 @@ class DeviceStepOps:
 
     def matvec(self, ap, boxes):
         """A(t) u on the owned planes of every shard (views into the output boxes); `boxes` are
-        box-sized vectors (owned planes valid) whose halos the exchange fills."""
+        box-sized vectors (owned planes valid) whose halos the exchange fills.  Returns (w, dots):
+        dots[i] = this shard's rows of u^H A u formed inside the fused kernel, or None when the
+        surrogate is outside its class (or a square-sum term is added outside it)."""
+        import torch
+
         nat = self.nat
+        ns = len(self.shards)
+        dots = [torch.zeros(2, dtype=torch.float64, device="cuda") for _ in range(ns)] if self.q == 0.0 else None
+        got = [False] * ns
         if self.exchange is None:
             for i, sh in enumerate(self.shards):
-                sh.apply_polynomial(self.appls[i], ap, boxes[i], self.outs[i], nat.HP_ADD_OSC)
+                got[i] = sh.apply_polynomial(self.appls[i], ap, boxes[i], self.outs[i], nat.HP_ADD_OSC,
+                                             dot=dots[i] if dots else None)
         else:  # emulated ranks: one exchange over all boxes, then the local matvecs
             self.exchange([sh.geo for sh in self.shards], boxes)
-            for i in range(len(self.shards)):
-                self.appls[i].apply_into(ap, boxes[i], self.outs[i], nat.HP_ADD_OSC)
-        w = [self.outs[i][self.own[i]] for i in range(len(self.shards))]
+            for i, sh in enumerate(self.shards):
+                g = sh.geo
+                if dots is not None and self.appls[i].apply_planes_into(ap, boxes[i], self.outs[i], g.lo - g.blo,
+                                                                        g.hi - g.blo, nat.HP_ADD_OSC, dot=dots[i]):
+                    got[i] = True
+                else:
+                    self.appls[i].apply_into(ap, boxes[i], self.outs[i], nat.HP_ADD_OSC)
+        w = [self.outs[i][self.own[i]] for i in range(ns)]
         if self.q != 0.0:
-            for i in range(len(self.shards)):
+            for i in range(ns):
                 w[i].add_(self.appls[i].apply_square_sum(boxes[i])[self.own[i]], alpha=self.q)
-        return w
+        return w, (dots if dots is not None and all(got) else None)
 
     def cdot(self, a, b):
         """per shard: a^H b as a float64 (re, im) tensor (fixed summation order)"""
@@ -309,7 +327,9 @@ def sharded_propagate(shards, fh, ys, t0: float, h: float, nsteps: int, m: int, 
     The basis is kept unnormalised (u_k = v_k / s_k with known s_k) and box-sized (the matvec
     reads it in place), so a Lanczos iteration is the sharded matvec on u_k, one dot and one
     fused update + norm pass (u_{k+1} = s_k A u_k - alpha_k s_k u_k - beta_{k-1} s_{k-1}
-    u_{k-1}); the step ends with one combine pass written over the state.  ``ops`` supplies
+    u_{k-1}); alpha comes out of the matvec itself when the fused kernel applies (its in-kernel
+    rows of u^H A u, hp_apply_polynomial_planes_dot), otherwise from one dot pass.  The step
+    ends with one combine pass written over the state.  ``ops`` supplies
     the per-shard kernels (default DeviceStepOps).  Returns ``ys`` advanced in place.
     """
     ops = ops or DeviceStepOps(shards, ys, fh, exchange)
@@ -331,8 +351,10 @@ def sharded_propagate(shards, fh, ys, t0: float, h: float, nsteps: int, m: int, 
         s = [1.0 / nrm0]
         alpha, beta = [], []
         for k in range(m):
-            w = ops.matvec(ap, UB[k])
-            alpha.append(s[k] * s[k] * float(total(ops.cdot(U[k], w))[0]))  # s_k^2 u_k^H A u_k
+            w, dots = ops.matvec(ap, UB[k])
+            if dots is None:  # the matvec did not form u_k^H A u_k itself
+                dots = ops.cdot(U[k], w)
+            alpha.append(s[k] * s[k] * float(total(dots)[0]))  # s_k^2 u_k^H A u_k
             if k == m - 1:
                 break
             nb = [ops.new_box(x) for x in ys]

@@ -120,7 +120,7 @@ class _CpuStepOps:
     def matvec(self, ap, boxes):
         halo_exchange(self.geo, boxes[0])
         y = self.appl.hamiltonian(ap.degrees, ap.coeffs, self.W.HALFWIDTH, boxes[0].numpy())
-        return [torch.from_numpy(y[self.geo.own_slice].copy())]
+        return [torch.from_numpy(y[self.geo.own_slice].copy())], None
 
     def cdot(self, a, b):
         d = np.vdot(a[0].numpy(), b[0].numpy())
