@@ -328,19 +328,35 @@ def gpu_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    # working sets that fit in L2 (cfg1, cfg2): every timed step is bracketed by its own events
+    # and L2 is flushed between steps (a 256 MB write outside the brackets), so no step reads
+    # what the previous one left in L2; larger working sets stream through HBM anyway
+    flush_l2 = algorithmic_bytes(w, n_local, batch) < 126e6  # in + out bytes vs the 126 MB L2
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush_l2 else None
     launches0 = nat.lib().hp_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
-        ev0.record()
-        for _ in range(args.steps):
-            step_dev()
-        ev1.record()
-        torch.cuda.synchronize()
+        if flush is None:
+            ev0.record()
+            for _ in range(args.steps):
+                step_dev()
+            ev1.record()
+            torch.cuda.synchronize()
+            ms = ev0.elapsed_time(ev1)
+        else:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for a, b in evs:
+                flush.fill_(1)
+                a.record()
+                step_dev()
+                b.record()
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in evs)
     launches = nat.lib().hp_launch_count() - launches0
-    ms = ev0.elapsed_time(ev1)
     ms_max = ms
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -418,8 +434,8 @@ def gpu_arm(args, rank, world, local_rank):
                 "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, SURVEY.md §8(d))",
                 "config": {"workload": w.name, "set": f"{w.kind} N={w.dim} bound={w.bound}", "n": sharding.global_size if sharding is not None else n_local,
                            "batch": w.batch, "nterms": int(ap.nterms), "halfwidth": W.HALFWIDTH,
-                           "l2": "inputs larger than L2 (no flush)" if alg_bytes / 2 > 126e6 else
-                           "working set L2-resident (not flushed)",
+                           "l2": "L2 flushed between steps (256 MB write outside the per-step events)" if flush_l2
+                           else "inputs larger than L2 (no flush)",
                            "parallelism": f"slab-j1 x{world}" if sharding is not None else
                            ("single" if world == 1 else f"batch/{world}" if part else f"replicas x{world}")},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
