@@ -668,3 +668,38 @@ def test_planes_fused_dot(hp, rng, bound):
     dot2 = torch.zeros(2, dtype=torch.float64, device="cuda")
     assert appl.apply_planes_into(ap, x, y, 6, side - 6, nat.HP_ADD_OSC, dot=dot2)
     assert torch.allclose(dot, dot2, rtol=1e-13, atol=0)
+
+
+_PERM_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1403_3511_b200 as hp
+from paper_1403_3511_b200 import workloads as W
+out = []
+for name, bound in (("cfg3", 255), ("cfg5", 63)):
+    w = W.CONFIGS[name].scaled(bound, name + "p")
+    s = hp.build_hyperbolic(w.dim, w.bound)
+    c = W.coefficients(w, s.indices)
+    out.append(hp.get_applier(s).apply_polynomial(w.approx(0.0), c))
+np.save(sys.argv[2], np.concatenate([np.ravel(o) for o in out]))
+"""
+
+
+def test_level_line_order_bitwise(tmp_path):
+    """The line-blocked traversal (HP_LEVEL_PERM, default axis 1) only reorders the level
+    kernels' work: matvec outputs on scaled cfg3 / cfg5 sets equal the ordinal-order run
+    (HP_LEVEL_PERM=0) bit for bit."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    outs = []
+    for env in ({}, {"HP_LEVEL_PERM": "0"}, {"HP_LEVEL_PERM": "7"}):
+        f = tmp_path / f"y{len(outs)}.npy"
+        r = subprocess.run([sys.executable, "-c", _PERM_SCRIPT, str(root), str(f)], env={**os.environ, **env},
+                           capture_output=True, text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
