@@ -169,6 +169,7 @@ struct CombineArgs {
   int nmix;
   double c0;
   int osc;
+  double sq;  // harmonic part q: q * sum_l x_l^2 folded into the single-axis bands (fast_apply.py:229-245)
 };
 
 // combined bands: P[a][j][d] = sum_k ws[a][k] B_{a,k}[j][d] (+ levels, + c0 on axis 4)
@@ -192,6 +193,12 @@ __global__ void k_fg_combine(const double* __restrict__ basis, double* __restric
           acc += A.ws[a][0];
           if (A.osc) acc += (double)(j + (a == 0 ? A.joff0 : 0)) + 0.5;
           if (a == 3) acc += A.c0;
+        }
+        if (A.sq != 0.0) {
+          const double jg = (double)(j + (a == 0 ? A.joff0 : 0));
+          if (d == FG_K) acc += A.sq * (jg + 0.5);
+          if (d == FG_K + 2 && j + 2 < n) acc += A.sq * 0.5 * sqrt((jg + 1.0) * (jg + 2.0));
+          if (d == FG_K - 2 && j >= 2) acc += A.sq * 0.5 * sqrt(jg * (jg - 1.0));
         }
       }
       P[(size_t)a * FG_MAXN * FG_W + rem] = acc;
@@ -488,11 +495,13 @@ size_t fullgrid_workspace_bytes(const hp_set_s* s, const std::vector<Term>& term
 // classification + band tables; *ok = false when the fused evaluator does not cover the call
 static hp_status fg_prepare(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                             int64_t batch, int flags, void* ws, size_t ws_bytes, cudaStream_t st, FgPlan* Fo,
-                            bool* ok) {
+                            bool* ok, double sq = 0.0) {
   *ok = false;
   FgPlan& F = *Fo;
   F = classify(s, terms, dtype, batch, flags);
   if (!F.ok) return HP_OK;
+  if (sq != 0.0)
+    for (int a = 0; a < 4; ++a) F.mask[a] |= (1u << (FG_K - 2)) | (1u << FG_K) | (1u << (FG_K + 2));
   size_t need = fullgrid_workspace_bytes(s, terms, dtype, batch, flags);
   if (ws_bytes < need) return HP_OK;  // caller sized for the generic program only
   hp_status rc = ensure_basis(s, halfwidth, st);
@@ -510,6 +519,7 @@ static hp_status fg_prepare(const hp_set_s* s, const std::vector<Term>& terms, d
   A.nmix = F.nmix;
   A.c0 = F.c0;
   A.osc = (flags & HP_ADD_OSC) ? 1 : 0;
+  A.sq = sq;
   k_fg_combine<<<64, 256, 0, st>>>(s->fg_basis, P, G, A);
   HP_LAUNCH_CHECK("k_fg_combine");
   *ok = true;
@@ -526,12 +536,12 @@ static bool fg_single_class(const FgPlan& F) {
 
 hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                          const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
-                         cudaStream_t st, bool* done, DotOut* dot) {
+                         cudaStream_t st, bool* done, DotOut* dot, double sq) {
   if (dot) dot->n = 0;
   *done = false;
   FgPlan F;
   bool ok = false;
-  hp_status rc = fg_prepare(s, terms, halfwidth, dtype, batch, flags, ws, ws_bytes, st, &F, &ok);
+  hp_status rc = fg_prepare(s, terms, halfwidth, dtype, batch, flags, ws, ws_bytes, st, &F, &ok, sq);
   if (rc || !ok) return rc;
   double* P = (double*)ws;
   double* G = P + 4 * FG_MAXN * FG_W;

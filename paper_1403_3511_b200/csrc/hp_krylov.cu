@@ -496,15 +496,24 @@ struct Hamiltonian {
   std::vector<Term> terms;
 };
 
+// the fused full-cube evaluator folds q * square_sum into its bands (*sq_done); the other
+// evaluators leave it to apply_ham_full
 static hp_status apply_ham(const Hamiltonian& H, const double2* v, double2* y, double2* ws, size_t ws_bytes,
-                           cudaStream_t st, DotOut* dot) {
+                           cudaStream_t st, DotOut* dot, bool* sq_done) {
   bool done = false;
+  *sq_done = false;
   hp_status rc = fullgrid_apply(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done,
-                                dot);
+                                dot, H.q);
   if (rc) return rc;
-  if (!done) rc = level_apply(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done, dot);
+  if (done) {
+    *sq_done = true;
+    return HP_OK;
+  }
+  DotOut* d = H.q == 0.0 ? dot : nullptr;
+  if (dot && !d) dot->n = 0;
+  rc = level_apply(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done, d);
   if (rc) return rc;
-  if (!done) rc = run_program<double2>(H.s, H.prog, H.halfwidth, v, y, 1, ws, ws_bytes, st, dot);
+  if (!done) rc = run_program<double2>(H.s, H.prog, H.halfwidth, v, y, 1, ws, ws_bytes, st, d);
   return rc;
 }
 
@@ -516,10 +525,10 @@ __global__ void k_axpy_c2(int64_t n, double c, const double2* __restrict__ x, do
 // A(t) v; if `dot` is given and the evaluator could fuse it, dot->n partials of <v, A v>
 static hp_status apply_ham_full(const Hamiltonian& H, const double2* v, double2* y, double2* tmp, double2* ws,
                                 size_t ws_bytes, cudaStream_t st, DotOut* dot = nullptr) {
-  hp_status rc = apply_ham(H, v, y, ws, ws_bytes, st, H.q == 0.0 ? dot : nullptr);
+  bool sq_done = false;
+  hp_status rc = apply_ham(H, v, y, ws, ws_bytes, st, dot, &sq_done);
   if (rc) return rc;
-  if (dot && H.q != 0.0) dot->n = 0;
-  if (H.q != 0.0) {
+  if (H.q != 0.0 && !sq_done) {
     rc = launch_square<double2>(H.s, v, tmp, 1, st);
     if (rc) return rc;
     int64_t n = H.s->n;

@@ -75,7 +75,7 @@ size_t fullgrid_workspace_bytes(const hp_set_s* s, const std::vector<Term>& term
                                 int64_t batch, int flags);
 hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                          const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
-                         cudaStream_t st, bool* done, DotOut* dot = nullptr);
+                         cudaStream_t st, bool* done, DotOut* dot = nullptr, double sq = 0.0);
 
 hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                                 const void* in, void* out, int plo, int phi, int flags, void* ws, size_t ws_bytes,

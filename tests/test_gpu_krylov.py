@@ -124,6 +124,30 @@ def test_harmonic_part_route_vs_oracle(hp):
     assert rel_l2(mv(c), want1) < TOL
 
 
+def test_harmonic_part_folded_full_cube(hp):
+    """harmonic_part != 0 on a cfg4-class full cube: q * square_sum rides in the fused evaluator's
+    single-axis bands (no separate square pass); Lanczos + propagation vs the oracle within 1e-12."""
+    from torch.profiler import ProfilerActivity, profile
+
+    w = W.CONFIGS["cfg4"].scaled(15, "cfg4q")
+    s = hp.build_full(w.dim, w.bound)
+    spec = hp.custom_potential(w.evaluator, w.dim, W.HALFWIDTH, harmonic_part=0.3)
+    fh = hp.FastHamiltonian(s, spec, w.degree)
+    c = W.coefficients(w)
+    appl = O.applier_for_full(w.dim, w.bound)
+    ham_at = O.hamiltonian_at(appl, w.evaluator, w.dim, W.HALFWIDTH, w.degree, harmonic_part=0.3)
+    want = O.propagate("midpoint", ham_at, c, 0.0, 0.015, 3, 7)
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        got = hp.propagate_magnus(hp.MagnusScheme.from_name("midpoint"), fh.matvec_at, c, 0.0, 0.015, 3, 7)
+    names = {e.key for e in prof.key_averages()}
+    assert not any("k_square" in k or "k_axpy_c2" in k for k in names), names
+    assert rel_l2(got, want) < TOL
+    fac = hp.lanczos(fh.matvec_at(0.01), c, 7)
+    ofac = O.lanczos(ham_at(0.01), c, 7)
+    assert rel_l2(fac.alpha, ofac.alpha) < 1e-13
+    assert rel_l2(fac.beta, ofac.beta) < 1e-13
+
+
 @pytest.mark.parametrize("bound,world", [(15, 2), (20, 4), (20, 3)])
 def test_sharded_propagation_emulated(bound, world):
     """Slab-sharded Magnus steps (sharding.sharded_propagate: owned-plane Lanczos with cross-shard
