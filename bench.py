@@ -392,9 +392,9 @@ def gpu_arm(args, rank, world, local_rank):
                 # result out, overlapped with the kernels (hp_apply_polynomial_streamed)
                 appl.apply_host_into(ap, xh, yh)
             else:
-                x.copy_(xh, non_blocking=True)
-                step_dev()
-                yh.copy_(y, non_blocking=True)
+                # this rank's box (owned + halo planes) of the host vector, streamed the same way:
+                # the halo comes with the host copy, so no device exchange (SlabShard.apply_host)
+                sharding.apply_host(appl, ap, xh, yh)
 
         step_e2e()
         torch.cuda.synchronize()
@@ -419,7 +419,9 @@ def gpu_arm(args, rank, world, local_rank):
                         ("j1-plane chunks, copies overlapped with the kernels)" if w.kind == "full" else
                          "groups of batch vectors, copies overlapped with the kernels)" if batch > 1 else
                          "whole-vector copies around the matvec)") if sharding is None else
-                        "pinned host -> HBM, hp_apply_polynomial (C ABI) + halo exchange, HBM -> pinned host")}
+                        "each rank: its slab box (owned + halo planes) of the pinned host vector -> HBM -> "
+                        "pinned host inside hp_apply_polynomial_streamed (C ABI; j1-plane chunks, copies "
+                        "overlapped with the kernels; the halo arrives with the host copy)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -181,6 +181,13 @@ class SlabShard:
             appl.apply_planes_into(ap, x, y, rng[1], hi, flags, dot=dot)
         return dot is not None
 
+    def apply_host(self, appl, ap, x_host, y_host, flags: int = 0) -> None:
+        """One matvec from host data: x_host is this rank's box of the host vector (owned planes
+        and halo planes, `local_coefficients`), so the halo arrives with the host->device copy and
+        no device exchange is needed.  One hp_apply_polynomial_streamed call: j1-plane chunks in,
+        kernels, chunks out, overlapped.  y_host[own_slice] is valid; halo rows are scratch."""
+        appl.apply_host_into(ap, x_host, y_host, flags)
+
 
 # ---------------------------------------------------------------- sharded time stepping
 

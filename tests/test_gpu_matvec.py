@@ -414,6 +414,30 @@ def test_slab_shards_on_device(hp, world):
 
 
 @pytest.mark.parametrize("world", [2, 3])
+def test_slab_shards_from_host(hp, world):
+    """SlabShard.apply_host (bench.py's sharded e2e leg): every rank streams its box of the host
+    vector through hp_apply_polynomial_streamed; the owned planes equal the full-cube matvec."""
+    import torch
+
+    from paper_1403_3511_b200.sharding import SlabShard
+
+    w = W.CONFIGS["cfg4"].scaled(31, "cfg4h")
+    ap = w.approx(0.3)
+    c = W.coefficients(w)
+    y_full = hp.get_applier(hp.build_full(w.dim, w.bound)).apply_polynomial(ap, c)
+    got = np.zeros_like(y_full)
+    for r in range(world):
+        s = SlabShard(w.dim, w.bound, r, world, halo=w.degree)
+        g = s.geo
+        xh = torch.from_numpy(s.local_coefficients(W, w)).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        s.apply_host(hp.get_applier(s.set), ap, xh, yh)
+        torch.cuda.synchronize()
+        got[g.lo * g.plane:g.hi * g.plane] = yh[g.own_slice].numpy()
+    assert rel_l2(got, y_full) < 1e-13
+
+
+@pytest.mark.parametrize("world", [2, 3])
 def test_slab_shards_overlapped(hp, world):
     """Overlapped shard schedule (interior planes while the halo is in flight, then the
     boundary planes): the interior pass reads owned planes only -- it is exact with poisoned
