@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_magnus(SmallArgs<AXS> A
   int* jt = (int*)((char*)dyn + vec_bytes);
   int* dnt = jt + A.dim * n;
   int* upt = dnt + A.dim * n;
-  double* sqt = (double*)(upt + A.dim * n);
+  double* sqt = (double*)(jt + (((size_t)3 * A.dim * n + 1) & ~(size_t)1));  // 8-byte aligned: 3 dim n may be odd
   if (use_tab) {
     for (int64_t o = t; o < n; o += SM_THREADS)
       for (int a = 0; a < A.dim; ++a) {
@@ -288,7 +288,7 @@ static hp_status small_magnus_step(const hp_set_s* s, const Program& p, double h
   size_t smem = (size_t)(std::max(p.nslots, 1) + 2) * s->n * sizeof(double2);
   if (smem > 200 * 1024) smem = 0;
   const int jmax = s->bound + 1;
-  const size_t tab = (size_t)s->dim * s->n * 3 * sizeof(int) + (size_t)(jmax + 2) * sizeof(double);
+  const size_t tab = (((size_t)s->dim * s->n * 3 + 1) & ~(size_t)1) * sizeof(int) + (size_t)(jmax + 2) * sizeof(double);
   const int use_tab = smem + tab <= 220 * 1024 ? 1 : 0;
   const size_t dyn = smem + (use_tab ? tab : 0);
   if (s->boxed) {
