@@ -215,3 +215,22 @@ def test_square_sum_diagonal_survives_pruning(hp):
     e[k] = 1.0
     out = hp.get_applier(s).apply_square_sum(e)
     assert out[k] == 3.0  # (1 + 1/2) + (1 + 1/2)
+
+
+@pytest.mark.parametrize("kind,dim,bound", [("full", 1, 10), ("full", 3, 6), ("hyp", 3, 9), ("hyp", 5, 7),
+                                            ("full", 2, 20)])
+def test_single_cta_propagation_odd_sizes(hp, kind, dim, bound):
+    """Small sets run the whole Magnus step in one CTA with shared-memory tables; sizes whose
+    table lengths are odd (n = 11, 343, ...) once misaligned the sqrt table.  3 midpoint steps
+    vs the oracle."""
+    s = hp.build_full(dim, bound) if kind == "full" else hp.build_hyperbolic(dim, bound)
+    idx = O.full_indices(dim, bound) if kind == "full" else O.hyperbolic_indices(dim, bound)
+    spec = hp.torsional(dim)
+    fh = hp.FastHamiltonian(s, spec, 4)
+    rng = np.random.default_rng(dim * 100 + bound)
+    c = rng.standard_normal(s.size) + 1j * rng.standard_normal(s.size)
+    c /= np.linalg.norm(c)
+    ham_at = O.hamiltonian_at(O.applier_for_set(idx), spec.evaluator, dim, 16.0, 4)
+    want = O.propagate("midpoint", ham_at, c, 0.0, 0.03, 3, 6)
+    got = hp.propagate_magnus(hp.MagnusScheme.from_name("midpoint"), fh.matvec_at, c, 0.0, 0.03, 3, 6)
+    assert rel_l2(got, want) < 1e-12
