@@ -234,3 +234,56 @@ def test_single_cta_propagation_odd_sizes(hp, kind, dim, bound):
     want = O.propagate("midpoint", ham_at, c, 0.0, 0.03, 3, 6)
     got = hp.propagate_magnus(hp.MagnusScheme.from_name("midpoint"), fh.matvec_at, c, 0.0, 0.03, 3, 6)
     assert rel_l2(got, want) < 1e-12
+
+
+@pytest.mark.parametrize("kind,dim,bound", [("full", 1, 0), ("hyp", 4, 1), ("full", 5, 1), ("hyp", 3, 2)])
+def test_degenerate_sets(hp, kind, dim, bound):
+    """One-element sets and 2^5 cubes: Hamiltonian matvec against the oracle bitwise in reference
+    order and within 1e-12 by default, and one Magnus step."""
+    s = hp.build_full(dim, bound) if kind == "full" else hp.build_hyperbolic(dim, bound)
+    idx = O.full_indices(dim, bound) if kind == "full" else O.hyperbolic_indices(dim, bound)
+    assert np.array_equal(s.indices, idx)
+
+    def ev(p, t):
+        y = p / 16.0
+        return (y ** 2).sum(axis=1) + 0.3 * y[:, 0] * y[:, -1] + 0.1 * y[:, 0] ** 3
+
+    spec = hp.custom_potential(ev, dim, 16.0)
+    ap = hp.interpolate(spec, 3)
+    rng = np.random.default_rng(dim + bound)
+    c = rng.standard_normal(s.size) + 1j * rng.standard_normal(s.size)
+    appl, oappl = hp.get_applier(s), O.applier_for_set(idx)
+    want = oappl.hamiltonian(ap.degrees, ap.coeffs, 16.0, c)
+    assert np.array_equal(appl.apply_hamiltonian(ap, c, ref_order=True), want)
+    assert rel_l2(appl.apply_hamiltonian(ap, c), want) < 1e-12
+    fh = hp.FastHamiltonian(s, spec, 3)
+    ham_at = O.hamiltonian_at(oappl, ev, dim, 16.0, 3)
+    c /= np.linalg.norm(c)
+    got = hp.propagate_magnus(hp.MagnusScheme.from_name("midpoint"), fh.matvec_at, c, 0.0, 0.02, 1, 4)
+    assert rel_l2(got, O.propagate("midpoint", ham_at, c, 0.0, 0.02, 1, 4)) < 1e-12
+
+
+@pytest.mark.parametrize("dim,bound", [(16, 2), (16, 5), (12, 8)])
+def test_widest_dimension_matvec(hp, dim, bound):
+    """The widest dimension the library takes (HP_MAXDIM = 16): hyperbolic sets bit-exact, and a
+    surrogate given as explicit terms (a tensor interpolation grid is out of reach at this width)
+    applied bitwise in reference order, within 1e-12 by default."""
+    from paper_1403_3511_b200.potential_approx import ChebApprox
+
+    s = hp.build_hyperbolic(dim, bound)
+    idx = O.hyperbolic_indices(dim, bound)
+    assert np.array_equal(s.indices, idx)
+    rng = np.random.default_rng(dim * bound)
+    degs = np.zeros((2 * dim + 3, dim), dtype=np.int64)
+    for a in range(dim):
+        degs[2 * a, a] = 2
+        degs[2 * a + 1, a] = 1
+    degs[2 * dim, [0, dim - 1]] = 1
+    degs[2 * dim + 1, [1, 2]] = [2, 1]
+    coeffs = rng.uniform(-0.5, 0.5, len(degs))
+    ap = ChebApprox(dim, 3, 16.0, 0.0, degs, coeffs, 0.0)
+    c = rng.standard_normal(s.size) + 1j * rng.standard_normal(s.size)
+    appl = hp.get_applier(s)
+    want = O.applier_for_set(idx).hamiltonian(degs, coeffs, 16.0, c)
+    assert np.array_equal(appl.apply_hamiltonian(ap, c, ref_order=True), want)
+    assert rel_l2(appl.apply_hamiltonian(ap, c), want) < 1e-12
