@@ -148,11 +148,13 @@ def test_harmonic_part_folded_full_cube(hp):
     assert rel_l2(fac.beta, ofac.beta) < 1e-13
 
 
-@pytest.mark.parametrize("bound,world", [(15, 2), (20, 4), (20, 3)])
-def test_sharded_propagation_emulated(bound, world):
+@pytest.mark.parametrize("bound,world,q", [(15, 2, 0.0), (20, 4, 0.0), (20, 3, 0.0), (15, 3, 0.3)])
+def test_sharded_propagation_emulated(bound, world, q):
     """Slab-sharded Magnus steps (sharding.sharded_propagate: owned-plane Lanczos with cross-shard
     reductions, the halo refreshed by every matvec), all ranks emulated in one process, against
-    the single-device propagation of the full cube: 3 midpoint steps, m = 7, within 1e-12."""
+    the single-device propagation of the full cube: 3 midpoint steps, m = 7, within 1e-12.  q != 0:
+    the harmonic square sum (folded into the fused bands on the single device, a separate pass
+    per shard)."""
     import torch
 
     import paper_1403_3511_b200 as hp
@@ -162,7 +164,7 @@ def test_sharded_propagation_emulated(bound, world):
     w = W.CONFIGS["cfg4"].scaled(bound, "cfg4p")
     c = W.coefficients(w)
     full = hp.build_full(w.dim, w.bound)
-    pot = hp.custom_potential(w.evaluator, w.dim, W.HALFWIDTH)
+    pot = hp.custom_potential(w.evaluator, w.dim, W.HALFWIDTH, harmonic_part=q)
     scheme = hp.MagnusScheme.from_name("midpoint")
     want = hp.FastHamiltonian(full, pot, w.degree).propagate(scheme, torch.from_numpy(c).cuda(), 0.0, w.dt, 3, 7)
     shards = [SlabShard(w.dim, w.bound, r, world, halo=w.degree) for r in range(world)]
