@@ -287,6 +287,9 @@ def gpu_arm(args, rank, world, local_rank):
     w = W.CONFIGS[args.workload]
     peaks, peak_kind = measured_peaks()
     hbm = float(peaks["hbm_gbs"])
+    if args.mode == "step":
+        step_mode(args, w, rank, world, local_rank, hbm, peak_kind)
+        return
 
     sharding = None
     if (world > 1 or args.force_shard) and w.kind == "full" and w.batch == 1:
@@ -371,13 +374,15 @@ def gpu_arm(args, rank, world, local_rank):
         total_coeffs = n_local * batch * world  # replicas: every rank did the whole workload
     value = total_coeffs / (ms_step * 1e-3)
 
-    # roofline of the matvec on this GPU: algorithmic bytes / step time
-    alg_bytes = algorithmic_bytes(w, n_local, batch)  # this rank's vectors
-    achieved = alg_bytes / (ms / args.steps * 1e-3) / 1e9
+    # roofline of the matvec per GPU: algorithmic bytes of ONE GPU's share of the step / the
+    # step time (max over ranks).  32 B per coefficient per vector; a slab rank counts only its
+    # owned planes (it writes only those), a batch rank its own vectors, a replica the whole set
+    alg_bytes = 32.0 * total_coeffs / world
+    achieved = alg_bytes / (ms_step * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": profiled_traffic(args.workload),
                 "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg_bytes,
-                "basis": "one full matvec (all its kernels) per step; 32 B/coefficient"}
+                "basis": "one full matvec (all its kernels) per step; 32 B/coefficient; per GPU, max-over-ranks time"}
 
     # e2e: pinned host buffers in, result back to host, timed on the device
     e2e = None
@@ -411,9 +416,12 @@ def gpu_arm(args, rank, world, local_rank):
             t = torch.tensor([ems], device=dev, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ems = float(t)
+        hb = torch.tensor([xh.numel() * xh.element_size(), yh.numel() * yh.element_size()], device=dev,
+                          dtype=torch.float64)
+        if world > 1:  # every rank's copies (slab boxes, batch parts or replicas)
+            torch.distributed.all_reduce(hb)
         e2e = {"value": total_coeffs / (ems * 1e-3), "unit": "coeffs/s",
-               "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
-               "d2h_bytes_per_step": int(yh.numel() * yh.element_size()), "ms_per_step": round(ems, 3),
+               "h2d_bytes_per_step": int(hb[0]), "d2h_bytes_per_step": int(hb[1]), "ms_per_step": round(ems, 3),
                "steps": e_steps,
                "path": ("pinned host -> HBM -> pinned host inside hp_apply_polynomial_streamed (C ABI; " +
                         ("j1-plane chunks, copies overlapped with the kernels)" if w.kind == "full" else
@@ -421,12 +429,23 @@ def gpu_arm(args, rank, world, local_rank):
                          "whole-vector copies around the matvec)") if sharding is None else
                         "each rank: its slab box (owned + halo planes) of the pinned host vector -> HBM -> "
                         "pinned host inside hp_apply_polynomial_streamed (C ABI; j1-plane chunks, copies "
-                        "overlapped with the kernels; the halo arrives with the host copy)")}
+                        "overlapped with the kernels; the halo arrives with the host copy, so this e2e figure "
+                        "excludes the NCCL halo exchange of the device-resident path)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = run_cpu(args.workload, 1, args.cpu_reps)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    # the named propagation run of the workload (cfg4: 50 midpoint steps at dt = 0.005), timed in
+    # the same process after the matvec buffers are released
+    prop = None
+    if w.nsteps > 0 and not args.no_prop:
+        del x, y
+        if not args.no_e2e:
+            del xh, yh
+        torch.cuda.empty_cache()
+        prop = propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind, sharding is not None)
 
     if rank == 0:
         line = {"metric": "Galerkin matvec throughput", "value": value, "unit": "coeffs/s", "n_gpus": world,
@@ -441,8 +460,126 @@ def gpu_arm(args, rank, world, local_rank):
                            "parallelism": f"slab-j1 x{world}" if sharding is not None else
                            ("single" if world == 1 else f"batch/{world}" if part else f"replicas x{world}")},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clk.summary()}
+                "clocks": clk.summary(), "propagation": prop}
         print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- propagation (time steps)
+
+def step_bytes(m: int, n: int) -> float:
+    """Algorithmic bytes of one midpoint Magnus step with m Krylov vectors: (112 m - 48) B per
+    coefficient: m matvecs at 32 B, m - 1 Lanczos updates at 64 B (read w, v_k,
+    v_(k-1), write v_(k+1)) and the final combine reading m vectors and writing one."""
+    return (112.0 * m - 48.0) * n
+
+
+def _cpu_step_sample(wname: str, m: int):
+    """The oracle's midpoint step on a bounded sample of the workload (same potential, same
+    per-coefficient work): cfg4 -> the K+1 = 32 cube (1.05M coefficients), cfg3 -> prod <= 1024
+    (611,556), cfg1 -> the full set."""
+    from oracle import hprop_oracle as O
+    from paper_1403_3511_b200 import workloads as W
+
+    w = W.CONFIGS[wname]
+    ws = {"cfg4": w.scaled(31), "cfg3": w.scaled(1023)}.get(wname, w)
+    if ws.kind == "full":
+        appl = O.applier_for_full(ws.dim, ws.bound)
+        c = W.coefficients(ws)
+    else:
+        idx = O.hyperbolic_indices(ws.dim, ws.bound)
+        appl = O.applier_for_set(idx)
+        c = W.coefficients(ws, idx)
+    ham_at = O.hamiltonian_at(appl, ws.evaluator, ws.dim, W.HALFWIDTH, ws.degree)
+    O.propagate("midpoint", ham_at, c, 0.0, ws.dt, 1, m)  # warm-up (surrogate caches)
+    k = 3 if ws.size() < 2_000_000 else 1
+    t0 = time.perf_counter()
+    O.propagate("midpoint", ham_at, c, 0.0, k * ws.dt, k, m)
+    sec = (time.perf_counter() - t0) / k
+    desc = (f"oracle port (hprop's numpy Lanczos/Magnus path) on {'the full set' if ws is w else ws.name}, "
+            f"n = {ws.size():,}, {k} midpoint step(s), m = {m}, 1 core")
+    return {"value": ws.size() / sec, "unit": "coeff-steps/s", "cores": 1, "kind": "port", "sample": desc,
+            "seconds_per_step": sec}
+
+
+def propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind, sharded):
+    """Time `args.prop_steps` midpoint Magnus steps (m = 7) of the workload's named run through the
+    public API with the state resident in HBM (FastHamiltonian.propagate at one GPU; the
+    slab-sharded sharded_propagate over NCCL when the matvec ran sharded), plus an e2e run of
+    propagate_magnus from a pinned host state back to a host state."""
+    import torch
+
+    import paper_1403_3511_b200 as hp
+    from paper_1403_3511_b200 import _native as nat
+    from paper_1403_3511_b200 import workloads as W
+
+    dev = torch.device("cuda", local_rank)
+    m = 7
+    nsteps = min(args.prop_steps, w.nsteps)
+    spec = hp.custom_potential(w.evaluator, w.dim, W.HALFWIDTH)
+    scheme = hp.MagnusScheme.from_name("midpoint")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if sharded:
+        from paper_1403_3511_b200.sharding import SlabShard, sharded_propagate
+
+        shard = SlabShard(w.dim, w.bound, rank, world, halo=w.degree)
+        g = shard.geo
+        yb = torch.zeros(g.box_size, dtype=torch.complex128, device=dev)
+        yb[g.own_slice] = torch.from_numpy(shard.local_coefficients(W, w)[g.own_slice]).to(dev)
+        fh = hp.FastHamiltonian(hp.build_full(w.dim, w.bound), spec, w.degree)
+        sharded_propagate([shard], fh, [yb.clone()], 0.0, w.dt, 2, m)  # warm-up
+        run = lambda k: sharded_propagate([shard], fh, [yb], 0.0, w.dt, k, m)  # noqa: E731
+        n = g.global_size
+    else:
+        s = build_set(hp, w)
+        c = W.coefficients(w, None if w.kind == "full" else s.indices)
+        fh = hp.FastHamiltonian(s, spec, w.degree)
+        yd = torch.from_numpy(c).to(dev)
+        fh.propagate(scheme, yd.clone(), 0.0, w.dt, 3, m)  # warm-up: workspace and term caches
+        run = lambda k: fh.propagate(scheme, yd, 0.0, w.dt, k, m)  # noqa: E731
+        n = s.size
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches0 = nat.lib().hp_launch_count()
+    with ClockSampler(local_rank, interval=0.01) as clk:
+        ev0.record()
+        run(nsteps)
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = nat.lib().hp_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / nsteps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t)
+    alg = step_bytes(m, n) / world
+    achieved = alg / (ms * 1e-3) / 1e9
+    out = {"workload": w.name, "scheme": "midpoint", "m": m, "dt": w.dt, "n": n, "steps": nsteps,
+           "named_run_steps": w.nsteps, "ms_per_step": round(ms, 4), "value": n / (ms * 1e-3),
+           "unit": "coeff-steps/s",
+           "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(achieved / hbm, 4), "peak_kind": peak_kind,
+                        "algorithmic_bytes_per_step": alg,
+                        "basis": f"(112 m - 48) B per coefficient-step at m = {m} (SURVEY §8(d)), per GPU"},
+           "gpu_launches": int(launches), "clocks": clk.summary(),
+           "parallelism": f"slab-j1 x{world}" if sharded else ("single" if world == 1 else f"replicas x{world}")}
+    if world == 1 and not sharded and not args.no_e2e:
+        # e2e: propagate_magnus on a host (numpy) state, as a reference user calls it: one copy
+        # in, the steps on the device, one copy out
+        ke = max(1, min(nsteps, 5))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        yh = hp.propagate_magnus(scheme, fh.matvec_at, c, 0.0, ke * w.dt, ke, m)
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / ke
+        out["e2e"] = {"value": n / (ems * 1e-3), "unit": "coeff-steps/s", "ms_per_step": round(ems, 3),
+                      "steps": ke, "h2d_bytes_per_step": int(c.nbytes / ke), "d2h_bytes_per_step": int(yh.nbytes / ke),
+                      "path": "propagate_magnus(midpoint, FastHamiltonian.matvec_at, numpy state): one copy in, "
+                              "the steps on the device, one copy out"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = _cpu_step_sample(w.name, m)
+    return out if rank == 0 else None
 
 
 def profiled_traffic(workload: str):
@@ -452,6 +589,26 @@ def profiled_traffic(workload: str):
         d = json.loads(p.read_text())
         return d.get(workload)
     return None
+
+
+def step_mode(args, w, rank, world, local_rank, hbm, peak_kind):
+    """--mode step: the named propagation run as the headline (one JSON line on rank 0)."""
+    if w.nsteps == 0:
+        raise SystemExit(f"{w.name} has no propagation run (cfg1, cfg3, cfg4 have)")
+    args.prop_steps = w.nsteps if args.steps == 20 else args.steps
+    sharded = (world > 1 or args.force_shard) and w.kind == "full" and w.batch == 1
+    p = propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind, sharded)
+    if rank != 0:
+        return
+    line = {"metric": "Magnus step throughput (midpoint, m = 7)", "value": p["value"], "unit": p["unit"],
+            "n_gpus": world, "steps": p["steps"], "warmup": 3, "ms_per_step": p["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong" if sharded or world == 1 else "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, SURVEY.md §8(d))",
+            "config": {"workload": w.name, "n": p["n"], "dt": w.dt, "m": p["m"], "parallelism": p["parallelism"],
+                       "l2": "inputs larger than L2 (no flush)" if p["n"] * 16 > 126e6 else "L2-resident state"},
+            "roofline": p["roofline"], "cpu_baseline": p.get("cpu_baseline"), "e2e": p.get("e2e"),
+            "gpu_launches": p["gpu_launches"], "clocks": p["clocks"]}
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -465,6 +622,11 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--mode", default="matvec", choices=["matvec", "step"],
+                    help="step: the named propagation run (cfg1/cfg3/cfg4) is the headline metric")
+    ap.add_argument("--no-prop", action="store_true", help="skip the propagation leg")
+    ap.add_argument("--prop-steps", type=int, default=10,
+                    help="Magnus steps timed in the propagation leg (capped at the named run's step count)")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the slab-sharded code path even at one rank (tests the N>1 path's local part)")
     args = ap.parse_args()

@@ -687,8 +687,10 @@ hp_status hp_apply_polynomial_streamed(hp_set_t s, const int32_t* degrees, const
   }
   cudaStream_t sin, sout;
   if ((rc = copy_streams(&sin, &sout))) return rc;
-  std::vector<cudaEvent_t> ev(2 * ng + 2);
-  for (auto& e : ev) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  StreamedEvents ev;
+  if ((rc = ev.create(2 * ng + 2))) return rc;
+  ev.drain[0] = sin;
+  ev.drain[1] = sout;
   HP_CUDA(cudaEventRecord(ev[2 * ng], st));  // after the caller's prior work
   HP_CUDA(cudaStreamWaitEvent(sin, ev[2 * ng], 0));
   HP_CUDA(cudaStreamWaitEvent(sout, ev[2 * ng], 0));
@@ -711,7 +713,7 @@ hp_status hp_apply_polynomial_streamed(hp_set_t s, const int32_t* degrees, const
   }
   HP_CUDA(cudaEventRecord(ev[2 * ng + 1], sout));
   HP_CUDA(cudaStreamWaitEvent(st, ev[2 * ng + 1], 0));
-  for (auto& e : ev) cudaEventDestroy(e);
+  ev.committed = true;
   return HP_OK;
 }
 

@@ -40,6 +40,31 @@ hp_status cuda_fail(cudaError_t e, const char* what);
     if (e_ != cudaSuccess) return hp::cuda_fail(e_, what); \
   } while (0)
 
+// Events of one streamed (host-buffer) call, destroyed on every exit path.  If the call fails
+// after queueing copies on the shared copy streams, the destructor drains those streams first,
+// so no queued copy still targets the caller's buffers when the error is returned.
+struct StreamedEvents {
+  std::vector<cudaEvent_t> ev;
+  cudaStream_t drain[2] = {nullptr, nullptr};
+  bool committed = false;
+  hp_status create(size_t n) {
+    ev.assign(n, nullptr);
+    for (auto& e : ev) {
+      cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      if (r != cudaSuccess) return cuda_fail(r, "cudaEventCreateWithFlags");
+    }
+    return HP_OK;
+  }
+  cudaEvent_t& operator[](size_t i) { return ev[i]; }
+  ~StreamedEvents() {
+    if (!committed)
+      for (cudaStream_t s : drain)
+        if (s) cudaStreamSynchronize(s);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);  // released once the recorded work completes
+  }
+};
+
 // ---------------------------------------------------------------- scalars
 __device__ __forceinline__ double zero_of(double) { return 0.0; }
 __device__ __forceinline__ double2 zero_of(double2) { return make_double2(0.0, 0.0); }

@@ -26,9 +26,6 @@
 // overlap only in part at 8 warps/SM.
 #pragma once
 
-#ifndef Q_CONST
-#define Q_CONST 0
-#endif
 #ifndef Q_FENCES
 #define Q_FENCES 0  // compiler fences between load phases: off measured 0.8% faster (2.416 vs 2.434 ms)
 #endif
@@ -61,62 +58,13 @@ constexpr unsigned Q_STAGE_BYTES = Q_STAGE * 16u;
 constexpr int Q_S = Q_STAGES;
 constexpr size_t Q_WOFF = (size_t)Q_S * Q_STAGE_BYTES;
 constexpr int Q_T1W = 8;  // doubles per axis-1 weight row
-constexpr size_t Q_TOFF = Q_WOFF + (Q_CONST ? 0 : (size_t)Q_MAXN * F1_WROW * sizeof(double));
-constexpr size_t Q_T2OFF = Q_TOFF + (Q_CONST ? 0 : (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double));
-constexpr size_t Q_T3OFF = Q_T2OFF + (Q_CONST ? 0 : (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double));
+constexpr size_t Q_TOFF = Q_WOFF + (size_t)Q_MAXN * F1_WROW * sizeof(double);
+constexpr size_t Q_T2OFF = Q_TOFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
+constexpr size_t Q_T3OFF = Q_T2OFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
 constexpr int Q_T3N = Q_MAXN + 16;  // axis-3 table: [5][Q_T3N], transposed (16 lanes read 128 B)
 constexpr size_t Q_BOFF = Q_T3OFF + (size_t)5 * Q_T3N * sizeof(double);
 constexpr int Q_TC = 64;  // tile codes cached in shared memory
 constexpr size_t Q_SMEM = Q_BOFF + 2 * Q_S * sizeof(uint64_t) + (Q_S + Q_TC) * sizeof(int);
-
-// Weight tables of the march axis (W rows) and of axes 1, 2 (T1, T2 rows), read through the
-// constant cache: every access is uniform over a warp (W: over the CTA; T1: a warp owns one
-// axis-1 row pair; T2: two rows per warp), so they cost neither registers nor shared-memory
-// wavefronts.  Filled per launch from the combined bands by k_fg_qtables + a stream-ordered copy.
-constexpr int Q_CW_W = 0;                                // [Q_MAXN][8]  march-axis rows
-constexpr int Q_CW_T1 = Q_CW_W + Q_MAXN * 8;             // [Q_MAXN + 8][8] axis-1 rows
-constexpr int Q_CW_T2 = Q_CW_T1 + (Q_MAXN + 8) * 8;      // [Q_MAXN + 8][8] axis-2 rows
-constexpr int Q_CW_N = Q_CW_T2 + (Q_MAXN + 8) * 8;
-__constant__ double q_cw[Q_CW_N];
-
-// rows: W[q]  = {P0(q,0), P0(q+2,-2), P0(q-2,2), P0(q+4,-4), P0(q-4,4), B0(q+1,-1), B0(q-1,1), 0}
-//       T1[r] = {P1(r,-4), P1(r,-2), P1(r,2), P1(r,4), G(r,-1), G(r,+1), P1(r,0), 0}
-//       T2[r] = {P2(r,-4), P2(r,-2), P2(r,2), P2(r,4), P2(r,0), 0, 0, 0}   (zeros past the cube)
-template <int NMIX>
-__device__ __forceinline__ void q_table_entry(double* out, int i, const double* P, const double* G, const double* B0,
-                                              int n0, int n1, int n2) {
-  const double* P0 = P;
-  const double* P1 = P + FG_MAXN * FG_W;
-  const double* P2 = P + 2 * FG_MAXN * FG_W;
-  const int e = i & 7;
-  double w = 0.0;
-  if (i < Q_CW_T1) {
-    const int q = i >> 3;
-    auto p0 = [&](int r, int d) { return (q < n0 && r >= 0 && r < n0) ? P0[r * FG_W + d + FG_K] : 0.0; };
-    auto b0 = [&](int r, int d) { return (NMIX && q < n0 && r >= 0 && r < n0) ? B0[r * FG_W + d + FG_K] : 0.0; };
-    const int rs[7] = {q, q + 2, q - 2, q + 4, q - 4, q + 1, q - 1};
-    const int ds[7] = {0, -2, 2, -4, 4, -1, 1};
-    if (e < 5) w = p0(rs[e], ds[e]);
-    else if (e < 7) w = b0(rs[e], ds[e]);
-  } else if (i < Q_CW_T2) {
-    const int r = (i - Q_CW_T1) >> 3;
-    const int ds[8] = {-4, -2, 2, 4, -1, 1, 0, 0};
-    if (r < n1 && e < 4) w = P1[r * FG_W + ds[e] + FG_K];
-    else if (r < n1 && e < 6) w = NMIX ? G[r * FG_W + ds[e] + FG_K] : 0.0;
-    else if (r < n1 && e == 6) w = P1[r * FG_W + FG_K];
-  } else {
-    const int r = (i - Q_CW_T2) >> 3;
-    const int ds[5] = {-4, -2, 2, 4, 0};
-    if (r < n2 && e < 5) w = P2[r * FG_W + ds[e] + FG_K];
-  }
-  out[i] = w;
-}
-template <int NMIX>
-__global__ void k_fg_qtables(double* __restrict__ out, const double* __restrict__ P, const double* __restrict__ G,
-                             const double* __restrict__ B0, int n0, int n1, int n2) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Q_CW_N; i += gridDim.x * blockDim.x)
-    q_table_entry<NMIX>(out, i, P, G, B0, n0, n1, n2);
-}
 
 __device__ __forceinline__ void q_prefetch4(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
   asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(
@@ -153,7 +101,6 @@ __global__ void __launch_bounds__(Q_NT, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-#if !Q_CONST
   // per-plane scatter weights (k_fg_single's row layout):
   // {P0(p,0), P0(p+2,-2), P0(p-2,2), P0(p+4,-4), P0(p-4,4), B0(p+1,-1), B0(p-1,1), 0}
   for (int q = tid; q < n0; q += Q_NT) {
@@ -194,7 +141,6 @@ __global__ void __launch_bounds__(Q_NT, 1)
     w[4] = ok ? P2[r * FG_W + FG_K] : 0.0;
     w[5] = w[6] = w[7] = 0.0;
   }
-#endif
   // axis-3 columns, transposed: T3w[i][r] = P3(r, -4, -2, 2, 4, 0 for i = 0..4)
   for (int r = tid; r < Q_T3N; r += Q_NT) {
     const bool ok = r < n3;
@@ -288,19 +234,11 @@ __global__ void __launch_bounds__(Q_NT, 1)
           const double2* st = stg + (size_t)cs * Q_STAGE;
           // march-axis weights of plane p (uniform over the CTA)
 #define Q3(i) A3[(i) * Q_T3N]
-#if Q_CONST
-#define QW(i) q_cw[Q_CW_W + p * 8 + (i)]
-#define QT1A(i) q_cw[Q_CW_T1 + J1 * 8 + (i)]
-#define QT1B(i) q_cw[Q_CW_T1 + J1 * 8 + 16 + (i)]
-#define QT2A(i) q_cw[Q_CW_T2 + J2 * 8 + (i)]
-#define QT2B(i) q_cw[Q_CW_T2 + J2 * 8 + 16 + (i)]
-#else
 #define QW(i) W[p * F1_WROW + (i)]
 #define QT1A(i) T1w[J1 * Q_T1W + (i)]
 #define QT1B(i) T1w[J1 * Q_T1W + 2 * Q_T1W + (i)]
 #define QT2A(i) T2w[J2 * Q_T1W + (i)]
 #define QT2B(i) T2w[J2 * Q_T1W + 2 * Q_T1W + (i)]
-#endif
           const double2 wa = make_double2(QW(0), QW(1));
           const double2 wc = make_double2(QW(4), QW(5));
           const double wd = QW(6);

@@ -219,7 +219,6 @@ __global__ void k_fg_combine(const double* __restrict__ basis, double* __restric
 #include "hp_fullgrid_kernels.cuh"
 #include "hp_fg1.cuh"
 #include "hp_fg4.cuh"
-#include "hp_fg4ri.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -294,15 +293,7 @@ static int fg_quad() {  // HP_FG_QUAD=0 selects the 512-point k_fg_single instea
   return v;
 }
 
-static bool fg_ri() {  // HP_FG_RI=1: split-component quad kernel (k_fg_quad_ri)
-  static int v = [] {
-    const char* e = getenv("HP_FG_RI");
-    return e && atoi(e) == 1 ? 1 : 0;
-  }();
-  return v == 1;
-}
-
-static int fg_np() {  // points per thread of the single-pass kernel (HP_FG_NP = 1 or 2)
+static int fg_np() {  // points per thread of k_fg_single (HP_FG_NP = 1 or 2)
   static int v = [] {
     const char* e = getenv("HP_FG_NP");
     return e && atoi(e) == 1 ? 1 : 2;
@@ -327,37 +318,7 @@ static int sm_count() {
   return n;
 }
 
-// The constant-bank weight tables (k_fg_quad with Q_CONST, k_fg_quad_ri) live in one per-device
-// buffer: their launches are serialised across streams -- each waits for the previous user's
-// kernel before the tables are overwritten.  The lock is held from staging to the launch.
-struct ConstTables {
-  std::unique_lock<std::mutex> lk;
-  cudaEvent_t done = nullptr;  // recorded after the kernel that reads the tables
-};
-template <int NMIX>
-static hp_status stage_const_tables(const hp_set_s* s, const double* P, const double* G, const double* B0,
-                                    cudaStream_t st, ConstTables* ct) {
-  static std::mutex mtx;
-  static cudaEvent_t ev[64] = {};
-  static double* stage[64] = {};
-  ct->lk = std::unique_lock<std::mutex>(mtx);
-  int dev = 0;
-  HP_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64) return HP_ERR_CUDA;
-  if (!ev[dev]) {
-    HP_CUDA(cudaEventCreateWithFlags(&ev[dev], cudaEventDisableTiming));
-    HP_CUDA(cudaMalloc(&stage[dev], Q_CW_N * sizeof(double)));
-  } else {
-    HP_CUDA(cudaStreamWaitEvent(st, ev[dev], 0));
-  }
-  k_fg_qtables<NMIX><<<(Q_CW_N + 255) / 256, 256, 0, st>>>(stage[dev], P, G, B0, s->side[0], s->side[1], s->side[2]);
-  HP_LAUNCH_CHECK("k_fg_qtables");
-  HP_CUDA(cudaMemcpyToSymbolAsync(q_cw, stage[dev], Q_CW_N * sizeof(double), 0, cudaMemcpyDeviceToDevice, st));
-  ct->done = ev[dev];
-  return HP_OK;
-}
-
-// k_fg_quad (default) or k_fg_quad_ri (HP_FG_RI=1): 8 x 8 x 16 tiles, sides <= Q_MAXN
+// k_fg_quad: 8 x 8 x 16 tiles, sides <= Q_MAXN
 template <int NMIX>
 static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, const double* P, const double* G,
                              const FgPlan& F, cudaStream_t st, DotOut* dot, bool* launched, int plo, int phi) {
@@ -371,27 +332,13 @@ static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, co
   const int grid = std::min(s->fg_ntiles4, sm_count());
   const bool use_dot = dot && dot->partial && grid <= dot->capacity;
   double2* dotp = use_dot ? dot->partial : nullptr;
-  const bool ri = fg_ri();
-  ConstTables ct;
-  if (Q_CONST || ri) {
-    if ((rc = stage_const_tables<NMIX>(s, P, G, B0, st, &ct))) return rc;
-  }
-  if (ri) {
-    auto kern = use_dot ? k_fg_quad_ri<NMIX, true> : k_fg_quad_ri<NMIX, false>;
-    HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QR_SMEM));
-    kern<<<grid, QR_NT, QR_SMEM, st>>>(mA1, mB2, v, y, P, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1], s->side[2],
-                                        s->side[3], dotp, plo, phi);
-    HP_LAUNCH_CHECK("k_fg_quad_ri");
-  } else {
-    auto kern = use_dot ? k_fg_quad<NMIX, true> : k_fg_quad<NMIX, false>;
-    HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
-    // exp = 0: k_fg_quad keeps the experiment slot of k_fg_single's signature (dropping it moves
-    // ptxas to a spilling allocation of the 255-register kernel)
-    kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
-                                     s->side[2], s->side[3], dotp, fg_exp(), plo, phi);
-    HP_LAUNCH_CHECK("k_fg_quad");
-  }
-  if (ct.done) HP_CUDA(cudaEventRecord(ct.done, st));
+  auto kern = use_dot ? k_fg_quad<NMIX, true> : k_fg_quad<NMIX, false>;
+  HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
+  // exp = 0: k_fg_quad keeps the experiment slot of k_fg_single's signature (dropping it moves
+  // ptxas to a spilling allocation of the 255-register kernel)
+  kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
+                                   s->side[2], s->side[3], dotp, fg_exp(), plo, phi);
+  HP_LAUNCH_CHECK("k_fg_quad");
   if (use_dot) dot->n = grid;
   *launched = true;
   return HP_OK;
@@ -699,8 +646,10 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
   const int nch = (n0 + C - 1) / C;
   cudaStream_t sin, sout;
   if ((rc = copy_streams(&sin, &sout))) return rc;
-  std::vector<cudaEvent_t> ev(2 * nch + 2);
-  for (auto& e : ev) HP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  StreamedEvents ev;
+  if ((rc = ev.create(2 * nch + 2))) return rc;
+  ev.drain[0] = sin;
+  ev.drain[1] = sout;
   cudaEvent_t ev0 = ev[2 * nch], evend = ev[2 * nch + 1];
   HP_CUDA(cudaEventRecord(ev0, st));  // orders the copies after the caller's prior work
   HP_CUDA(cudaStreamWaitEvent(sin, ev0, 0));
@@ -728,7 +677,7 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
   }
   HP_CUDA(cudaEventRecord(evend, sout));
   HP_CUDA(cudaStreamWaitEvent(st, evend, 0));
-  for (auto& e : ev) cudaEventDestroy(e);  // released once the recorded work completes
+  ev.committed = true;
   *done = true;
   return HP_OK;
 }

@@ -147,6 +147,8 @@ class FastHamiltonian:
     def _step(self, approxes, y, h, m, reorth, want_fac):
         import torch
 
+        if want_fac:
+            return self._step_with_factorization(approxes, y, h, m, reorth)
         ydev, host = self._vec(y)
         if float(torch.linalg.vector_norm(ydev)) == 0.0:
             raise ValueError("starting vector must be nonzero")
@@ -155,12 +157,38 @@ class FastHamiltonian:
         d = diag.cpu().numpy()
         if d[3] != 0:
             raise RuntimeError("tridiagonal QL failed to converge")
-        out = ydev.cpu().numpy() if host else ydev
-        if not want_fac:
-            return out
-        fac = LanczosFactorization(None, np.zeros(int(d[0])), np.zeros(max(int(d[0]) - 1, 0)),
-                                   None if d[2] < 0 else int(d[2]), float(d[1]))
-        return out, fac
+        return ydev.cpu().numpy() if host else ydev
+
+    def _step_with_factorization(self, approxes, y, h, m, reorth):
+        """exp(-i h B) y together with the Lanczos factorization it was built from.
+
+        The reference returns the real factorization (krylov_propagator.py:180-186, 237-244) and
+        its callers read it (basis columns, alpha, beta).  The fused step keeps only scaled,
+        unnormalised basis vectors, so this path runs the device Lanczos (hp_lanczos, normalised
+        basis; or the generic device recurrence over the GL2 operator) and forms
+        ||y|| V exp(-i h T) e_1 from it, exactly the reference's sequence.
+        """
+        import torch
+
+        from .krylov_propagator import _expm_col_dev, _lanczos_generic
+
+        ydev, host = self._vec(y)
+        if len(approxes) == 1:
+            fac = _HamMatVec(self, approxes[0]).lanczos(ydev, m, reorthogonalize=reorth)
+        else:
+            a1, a2 = _HamMatVec(self, approxes[0]), _HamMatVec(self, approxes[1])
+            gamma = _SQRT3 / 12.0 * h
+
+            def gl2(v):
+                y1, y2 = a1(v), a2(v)
+                return 0.5 * (y1 + y2) - 1j * gamma * (a2(y1) - a1(y2))
+
+            fac = _lanczos_generic(gl2, ydev, m, reorth)
+        col = _expm_col_dev(fac.alpha, fac.beta, h)
+        out = float(torch.linalg.vector_norm(ydev)) * (fac.basis @ col)
+        return (out.cpu().numpy() if host else out), LanczosFactorization(
+            fac.basis.cpu().numpy() if host else fac.basis, fac.alpha, fac.beta, fac.breakdown_at,
+            fac.hermiticity_defect)
 
     def _approxes(self, scheme: MagnusScheme, t: float, h: float):
         if scheme.name == "midpoint":
@@ -186,7 +214,12 @@ class FastHamiltonian:
             t = t0 + k * h
             self._step_dev(self._approxes(scheme, t, h), ydev, h, m, reorthogonalize, diag[k])
             if callback is not None:
-                callback(k + 1, t + h, ydev.cpu().numpy() if host else ydev)
+                # the reference raises at the failing step, before its callback sees the state;
+                # the callback already costs a sync, so the QL flag is checked here per step.  Each
+                # call gets its own array/tensor (the device state is overwritten in place)
+                if float(diag[k, 3]) != 0:
+                    raise RuntimeError("tridiagonal QL failed to converge")
+                callback(k + 1, t + h, ydev.cpu().numpy() if host else ydev.clone())
         if bool((diag[:, 3] != 0).any()):
             raise RuntimeError("tridiagonal QL failed to converge")
         self.last_diagnostics = diag

@@ -298,7 +298,18 @@ def install(iset) -> PolynomialApplier:
     FastHamiltonian route through the device (fast_apply.py:250-253).  The
     reference set's indices are uploaded once as a custom device set.
     """
-    dev = IndexSet(iset.dim, iset.bound, "custom", np.asarray(iset.indices))
+    from .index_set import build_full, build_hyperbolic
+
+    ref_idx = np.asarray(iset.indices)
+    dev = None
+    if iset.kind in ("full", "hyperbolic"):
+        # the structured device set (stride arithmetic / unranking kernels, and on full cubes the
+        # fused single-pass evaluator) when it is the same member list in the same order
+        cand = (build_full if iset.kind == "full" else build_hyperbolic)(iset.dim, iset.bound)
+        if cand.size == ref_idx.shape[0] and np.array_equal(cand.indices, ref_idx):
+            dev = cand
+    if dev is None:
+        dev = IndexSet(iset.dim, iset.bound, "custom", ref_idx)
     appl = PolynomialApplier(dev)
     iset._derived["applier"] = appl
     return appl

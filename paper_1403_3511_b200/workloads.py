@@ -197,9 +197,45 @@ def coefficients(w: Workload, indices: np.ndarray | None = None, chunk: int = 1 
     # norms by numpy's pairwise summation (not BLAS dot, whose result depends
     # on the host's OpenBLAS thread count): identical inputs on every machine
     for r in range(rows.shape[0]):
-        sq = 0.0
-        for s in range(0, n, chunk):
-            blk = rows[r, s:min(n, s + chunk)]
-            sq += float(np.sum(blk.real * blk.real) + np.sum(blk.imag * blk.imag))
-        rows[r] /= math.sqrt(sq)
+        _normalise(rows[r], chunk)
     return c
+
+
+def _normalise(row: np.ndarray, chunk: int) -> None:
+    n = row.shape[0]
+    sq = 0.0
+    for s in range(0, n, chunk):
+        blk = row[s:min(n, s + chunk)]
+        sq += float(np.sum(blk.real * blk.real) + np.sum(blk.imag * blk.imag))
+    row /= math.sqrt(sq)
+
+
+def coefficients_row(w: Workload, indices: np.ndarray | None, row: int, chunk: int = 1 << 24) -> np.ndarray:
+    """Row ``row`` of ``coefficients(w, indices)``, bit-identical, without the whole batch.
+
+    The seeded stream is drawn in the same chunks as ``coefficients`` and the
+    draws of the other rows are discarded (cfg5: 0.4 GB instead of 13 GB).
+    """
+    n = w.size()
+    if not 0 <= row < w.batch:
+        raise ValueError("row out of range")
+    rng = np.random.default_rng([w.seed, 0])
+    total = w.batch * n
+    out = np.empty(n, dtype=np.complex128)
+    lo, hi = row * n, (row + 1) * n
+    for part in ("re", "im"):
+        for s in range(0, total, chunk):
+            e = min(total, s + chunk)
+            vals = rng.standard_normal(e - s)
+            a, b = max(s, lo), min(e, hi)
+            if a < b:
+                if part == "re":
+                    out.real[a - lo:b - lo] = vals[a - s:b - s]
+                else:
+                    out.imag[a - lo:b - lo] = vals[a - s:b - s]
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        idx = _full_rows(w.dim, w.bound, s, e) if w.kind == "full" else indices[s:e]
+        out[s:e] *= decay_values(w.decay, idx)
+    _normalise(out, chunk)
+    return out
