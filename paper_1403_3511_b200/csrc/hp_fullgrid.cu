@@ -257,15 +257,22 @@ static hp_status make_tiles(const hp_set_s* s, int T1, int T2, int T3, int** out
   std::lock_guard<std::mutex> g(s->fg_mtx);
   if (*out) return HP_OK;
   const int t1 = (s->side[1] + T1 - 1) / T1, t2 = (s->side[2] + T2 - 1) / T2, t3 = (s->side[3] + T3 - 1) / T3;
-  int BE = 3;  // block edge in tiles (HP_FG_BLOCK overrides)
-  if (const char* e = getenv("HP_FG_BLOCK")) BE = std::max(1, atoi(e));
+  // blocks of E1 x E2 x E3 tiles (axis 3 fastest inside a block); HP_FG_BLOCK = "e" or "e1,e2,e3"
+  int E[3] = {3, 3, t3};
+  if (const char* e = getenv("HP_FG_BLOCK")) {
+    int a = 0, b = 0, c = 0;
+    const int k = sscanf(e, "%d,%d,%d", &a, &b, &c);
+    if (k == 1) E[0] = E[1] = std::max(1, a);
+    if (k == 3) E[0] = std::max(1, a), E[1] = std::max(1, b), E[2] = std::max(1, c);
+  }
   std::vector<int> codes;
   codes.reserve((size_t)t1 * t2 * t3);
-  for (int b1 = 0; b1 < t1; b1 += BE)
-    for (int b2 = 0; b2 < t2; b2 += BE)
-      for (int i1 = b1; i1 < std::min(t1, b1 + BE); ++i1)
-        for (int i2 = b2; i2 < std::min(t2, b2 + BE); ++i2)
-          for (int i3 = 0; i3 < t3; ++i3) codes.push_back(i1 | (i2 << 10) | (i3 << 20));
+  for (int b1 = 0; b1 < t1; b1 += E[0])
+    for (int b2 = 0; b2 < t2; b2 += E[1])
+      for (int b3 = 0; b3 < t3; b3 += E[2])
+        for (int i1 = b1; i1 < std::min(t1, b1 + E[0]); ++i1)
+          for (int i2 = b2; i2 < std::min(t2, b2 + E[1]); ++i2)
+            for (int i3 = b3; i3 < std::min(t3, b3 + E[2]); ++i3) codes.push_back(i1 | (i2 << 10) | (i3 << 20));
   int* d = nullptr;
   HP_CUDA(cudaMalloc(&d, codes.size() * sizeof(int)));
   HP_CUDA(cudaMemcpy(d, codes.data(), codes.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -309,6 +316,24 @@ static int fg_exp() {  // timing experiments only (HP_FG_EXP bit 0: skip halo bo
   return v;
 }
 
+static int fg_sync() {  // plane lock-step slack of k_fg_quad (HP_FG_SYNC; 0 = free-running)
+  static int v = [] {
+    const char* e = getenv("HP_FG_SYNC");
+    return e ? std::max(0, atoi(e)) : 0;
+  }();
+  return v;
+}
+// per-set progress counters of the lock-step march (rounds x planes ints)
+static hp_status ensure_prog(const hp_set_s* s, size_t count) {
+  std::lock_guard<std::mutex> g(s->fg_mtx);
+  if (s->fg_prog && s->fg_prog_n >= count) return HP_OK;
+  if (s->fg_prog) HP_CUDA(cudaFree(s->fg_prog));
+  s->fg_prog = nullptr;
+  HP_CUDA(cudaMalloc(&s->fg_prog, count * sizeof(int)));
+  s->fg_prog_n = count;
+  return HP_OK;
+}
+
 static int sm_count() {
   static int n = [] {
     int dev = 0, c = 148;
@@ -336,8 +361,16 @@ static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, co
   HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
   // exp = 0: k_fg_quad keeps the experiment slot of k_fg_single's signature (dropping it moves
   // ptxas to a spilling allocation of the 255-register kernel)
+  int* prog = nullptr;
+  const int sync_d = fg_sync();
+  if (sync_d > 0) {
+    const size_t items = (size_t)((s->fg_ntiles4 + grid - 1) / grid) * n0;  // >= items per CTA
+    if ((rc = ensure_prog(s, items))) return rc;
+    prog = s->fg_prog;
+    HP_CUDA(cudaMemsetAsync(prog, 0, items * sizeof(int), st));
+  }
   kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
-                                   s->side[2], s->side[3], dotp, fg_exp(), plo, phi);
+                                   s->side[2], s->side[3], dotp, fg_exp(), plo, phi, prog, sync_d);
   HP_LAUNCH_CHECK("k_fg_quad");
   if (use_dot) dot->n = grid;
   *launched = true;
