@@ -186,8 +186,6 @@ struct hp_set_s {
   mutable int fg_ntiles = 0;
   // the same for the quad kernel's 8 x 8 x 16 tiles (hp_fg4.cuh)
   mutable int* fg_tiles4 = nullptr;
-  mutable int* fg_prog = nullptr;  // k_fg_quad lock-step progress counters
-  mutable size_t fg_prog_n = 0;
   mutable int fg_ntiles4 = 0;
   // tabled sets: per-axis line order (ordinals grouped by axis line, hp_level.cu), built on
   // first use by the level kernels of outer axes

@@ -78,8 +78,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
     k_fg_quad(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB2,
               const double2* __restrict__ v, double2* __restrict__ y, const double* __restrict__ P,
               const double* __restrict__ G, const double* __restrict__ B0, const int* __restrict__ tiles, int ntiles,
-              int n0, int n1, int n2, int n3, double2* __restrict__ dotp, int exp, int plo, int phi,
-              int* __restrict__ prog, int sync_d) {
+              int n0, int n1, int n2, int n3, double2* __restrict__ dotp, int exp, int plo, int phi) {
   extern __shared__ __align__(128) unsigned char q_smem[];
   double2* stg = (double2*)q_smem;
   double* W = (double*)(q_smem + Q_WOFF);
@@ -176,15 +175,6 @@ __global__ void __launch_bounds__(Q_NT, 1)
     f1_tma4_hint(dst + Q_OFF_LO, &mB2, 2 * T3, T2 - Q_H, T1, pp, bar, pol);
     f1_tma4_hint(dst + Q_OFF_HI, &mB2, 2 * T3, T2 + Q_T2, T1, pp, bar, pol);
   };
-  // Plane lock-step (prog != nullptr): the CTAs of one tile round march j1 together, at most
-  // sync_d planes apart, so a tile's halo rows -- the neighbours' own rows -- are still in L2
-  // when it reads them (free-running CTAs drift apart and re-read halos from DRAM).  Every CTA
-  // walks the same item sequence k = round * nper + plane, so prog[k] counts the CTAs that
-  // released item k; the refill of item k waits until all CTAs holding item k - sync_d have
-  // released it.  Bounded spin: a CTA that times out (CTAs not co-resident) stops waiting.
-  int spins_left = 1 << 14;
-  const int full_items = (ntiles / (int)gridDim.x) * nper;  // items every CTA has
-  const int last_cnt = ntiles % (int)gridDim.x;              // CTAs in the partial last round
   if (tid == 0)
     for (int k = 0; k < min(Q_S, nitems); ++k) issue_item(k, k);
   int kk = 0;  // this thread's item index
@@ -371,15 +361,6 @@ __global__ void __launch_bounds__(Q_NT, 1)
             if (atomicAdd(&cnt[cs], 1) == Q_NT / 32 - 1) {
               cnt[cs] = 0;
               f1_mbar_wait(&empty[cs], (unsigned)(cu & 1));  // all releases landed (acquire)
-              if (prog) {
-                atomicAdd(prog + kk, 1);
-                const int q = kk + Q_S - sync_d;
-                if (kk + Q_S < nitems && q >= 0 && spins_left > 0) {
-                  const int target = q < full_items ? (int)gridDim.x : last_cnt;
-                  const volatile int* pc = prog + q;
-                  while (*pc < target && --spins_left > 0) __nanosleep(64);
-                }
-              }
               if (kk + Q_S < nitems) issue_item(kk + Q_S, cs);
             }
           }

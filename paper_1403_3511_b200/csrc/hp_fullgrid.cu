@@ -316,24 +316,6 @@ static int fg_exp() {  // timing experiments only (HP_FG_EXP bit 0: skip halo bo
   return v;
 }
 
-static int fg_sync() {  // plane lock-step slack of k_fg_quad (HP_FG_SYNC; 0 = free-running)
-  static int v = [] {
-    const char* e = getenv("HP_FG_SYNC");
-    return e ? std::max(0, atoi(e)) : 0;
-  }();
-  return v;
-}
-// per-set progress counters of the lock-step march (rounds x planes ints)
-static hp_status ensure_prog(const hp_set_s* s, size_t count) {
-  std::lock_guard<std::mutex> g(s->fg_mtx);
-  if (s->fg_prog && s->fg_prog_n >= count) return HP_OK;
-  if (s->fg_prog) HP_CUDA(cudaFree(s->fg_prog));
-  s->fg_prog = nullptr;
-  HP_CUDA(cudaMalloc(&s->fg_prog, count * sizeof(int)));
-  s->fg_prog_n = count;
-  return HP_OK;
-}
-
 static int sm_count() {
   static int n = [] {
     int dev = 0, c = 148;
@@ -361,16 +343,8 @@ static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, co
   HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
   // exp = 0: k_fg_quad keeps the experiment slot of k_fg_single's signature (dropping it moves
   // ptxas to a spilling allocation of the 255-register kernel)
-  int* prog = nullptr;
-  const int sync_d = fg_sync();
-  if (sync_d > 0) {
-    const size_t items = (size_t)((s->fg_ntiles4 + grid - 1) / grid) * n0;  // >= items per CTA
-    if ((rc = ensure_prog(s, items))) return rc;
-    prog = s->fg_prog;
-    HP_CUDA(cudaMemsetAsync(prog, 0, items * sizeof(int), st));
-  }
   kern<<<grid, Q_NT, Q_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles4, s->fg_ntiles4, n0, s->side[1],
-                                   s->side[2], s->side[3], dotp, fg_exp(), plo, phi, prog, sync_d);
+                                   s->side[2], s->side[3], dotp, fg_exp(), plo, phi);
   HP_LAUNCH_CHECK("k_fg_quad");
   if (use_dot) dot->n = grid;
   *launched = true;

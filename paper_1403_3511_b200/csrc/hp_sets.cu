@@ -502,7 +502,6 @@ hp_status hp_set_destroy(hp_set_t s) {
   if (s->fg_basis) cudaFree(s->fg_basis);
   if (s->fg_tiles) cudaFree(s->fg_tiles);
   if (s->fg_tiles4) cudaFree(s->fg_tiles4);
-  if (s->fg_prog) cudaFree(s->fg_prog);
   delete s;
   return HP_OK;
 }
