@@ -162,6 +162,30 @@ hp_status hp_apply_polynomial_planes_dot(hp_set_t s, const int32_t* degrees_host
 hp_status hp_square_sum(hp_set_t s, int dtype, const void* in_dev, void* out_dev,
                         int64_t batch, void* stream);
 
+/* ---- full cube <-> subset maps (index_set.py:296-319, error_lab.py:114-148) ---- */
+
+/* restrict -- index_set.py:308-311: sub[o] = full[pos(o)] for each of `batch` vectors, pos(j) =
+ * sum_l j_l (bound+1)^(dim-l) computed on the device from the subset's tables.  `full` must be
+ * a full cube (not a slab) of the subset's (dim, bound): HP_ERR_VALUE "target of
+ * restrict/extend must be a full cube" / "set mismatch: ..." otherwise. */
+hp_status hp_restrict(hp_set_t subset, hp_set_t full, int dtype, const void* full_dev, void* sub_dev,
+                      int64_t batch, void* stream);
+
+/* extend -- index_set.py:314-319: full = 0, then full[pos(o)] = sub[o]. */
+hp_status hp_extend(hp_set_t subset, hp_set_t full, int dtype, const void* sub_dev, void* full_dev,
+                    int64_t batch, void* stream);
+
+/* reduction_error's components -- error_lab.py:114-130: comp[o] = |on_set[o] - on_full[pos(o)]|
+ * (float64 out; the restrict and the difference in one pass). */
+hp_status hp_reduction_components(hp_set_t subset, hp_set_t full, int dtype, const void* on_set_dev,
+                                  const void* on_full_dev, double* comp_dev, void* stream);
+
+/* reduction_local_mask -- error_lab.py:133-148: mask[o] = 1 iff j(o) + r is in the set for every
+ * degree tuple r of the term list (up-walks through the neighbour tables; bound test on cubes).
+ * Synchronises the stream. */
+hp_status hp_reduction_local_mask(hp_set_t s, const int32_t* degrees_host, int nterms, uint8_t* mask_dev,
+                                  void* stream);
+
 /* ---- Lanczos / Magnus (krylov_propagator.py) ---------------------------- */
 
 /* One exponential Magnus step y <- exp(-i h B) y via an m-step Lanczos

@@ -17,7 +17,8 @@ from .fast_apply import (PolynomialApplier, apply_hamiltonian, cheb_of_coordinat
                          fast_algorithm, get_applier, install, square_sum_apply)
 from .krylov_propagator import (LanczosFactorization, MagnusScheme, expm_tridiag_column, lanczos,
                                 lanczos_exp_apply, magnus_step, propagate_magnus, tridiag_eigh)
-from .error_lab import FastHamiltonian, make_decay_vector
+from .error_lab import (MEASURE_REDUCTION, ErrorReport, FastHamiltonian, make_decay_vector, reduction_error,
+                        reduction_local_mask)
 
 __version__ = "0.1.0"
 

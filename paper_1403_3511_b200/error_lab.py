@@ -1,8 +1,10 @@
 """Hamiltonian glue for the propagation loop (drop-in for hprop.error_lab.FastHamiltonian).
 
-Only the hot-path pieces of pkg/src/hprop/error_lab.py are mirrored:
-`FastHamiltonian` (error_lab.py:154-185) and `make_decay_vector`
-(error_lab.py:43-56).  The error studies are out of scope.
+Mirrored from pkg/src/hprop/error_lab.py: `FastHamiltonian` (error_lab.py:154-185),
+`make_decay_vector` (:43-56) and the reduction-error measurement that runs the same device
+matvec on the set and on its full cube -- `reduction_error`, `reduction_local_mask`,
+`ErrorReport` (:59-79, :114-148).  The quadrature and Lanczos
+perturbation studies (dense assembled matrices) are out of scope.
 
 A(t) = D + W_pol(t) [+ q * sum_l x_l^2 through the exact banded entries],
 with W_pol the Chebyshev surrogate of the smooth remainder of the potential.
@@ -19,10 +21,96 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
-from .fast_apply import _term_arrays, get_applier
-from .index_set import CoeffVector, IndexSet, _is_torch
+from .fast_apply import _term_arrays, fast_algorithm, get_applier
+from .index_set import CoeffVector, IndexSet, _is_torch, build_full, extend
 from .krylov_propagator import LanczosFactorization, MagnusScheme, _SQRT3
 from .potential_approx import ChebApprox, PotentialSpec, interpolate, smooth_remainder
+
+
+MEASURE_QUADRATURE = "quadrature"
+MEASURE_REDUCTION = "reduction"
+
+
+@dataclass(frozen=True)
+class ErrorReport:
+    """Per-index error magnitudes over a set with provenance (error_lab.py:59-79).
+
+    ``components`` is a float64 array (numpy, or a CUDA tensor when the input vector was one).
+    """
+
+    iset: IndexSet
+    components: object
+    metadata: dict
+
+    def _host(self) -> np.ndarray:
+        c = self.components
+        return c.cpu().numpy() if _is_torch(c) else np.asarray(c)
+
+    @property
+    def max_norm(self) -> float:
+        c = self._host()
+        return float(c.max()) if c.size else 0.0
+
+    def write_csv(self, path) -> None:
+        """Sorted ``# key=value`` metadata lines, ``# max_norm``, then k_1..k_N,magnitude rows."""
+        lines = [f"# {k}={self.metadata[k]}\n" for k in sorted(self.metadata)]
+        lines.append(f"# max_norm={self.max_norm:.17g}\n")
+        lines.append(",".join([f"k_{a + 1}" for a in range(self.iset.dim)] + ["magnitude"]) + "\n")
+        rows = self.iset.indices.tolist()
+        lines.extend(",".join(map(str, r)) + f",{m:.17g}\n" for r, m in zip(rows, self._host()))
+        with open(path, "w", newline="\n") as fh:
+            fh.write("".join(lines))
+
+
+def _metadata(iset: IndexSet, approx: ChebApprox, measure: str, **extra) -> dict:
+    md = dict(measure=measure, dim=iset.dim, bound=iset.bound, set_kind=iset.kind, set_size=iset.size,
+              degree=approx.degree, halfwidth=approx.halfwidth, nterms=approx.nterms)
+    md.update(extra)
+    return md
+
+
+def reduction_error(iset: IndexSet, approx: ChebApprox, v: CoeffVector, *,
+                    full: IndexSet | None = None) -> ErrorReport:
+    """|fast(set) v - restrict(fast(cube) extend(v))| per index (error_lab.py:114-130).
+
+    Both applications are the device matvec; extend is a device scatter and the final
+    restrict-and-subtract is one fused kernel (hp_reduction_components).  Components stay on the
+    device when v does.
+    """
+    import torch
+
+    if full is None:
+        full = build_full(iset.dim, iset.bound)
+    on_set = fast_algorithm(iset, approx, v).data
+    on_full = fast_algorithm(full, approx, extend(v, full)).data
+    host = not _is_torch(on_set)
+    a = torch.from_numpy(np.ascontiguousarray(on_set)).cuda() if host else on_set.contiguous()
+    b = torch.from_numpy(np.ascontiguousarray(on_full)).cuda() if host else on_full.contiguous()
+    if a.dtype != b.dtype:
+        common = torch.promote_types(a.dtype, b.dtype)
+        a, b = a.to(common), b.to(common)
+    a = iset._to_canon(a)  # the fused kernel walks the set's device (canonical) order
+    comp = torch.empty(iset.size, dtype=torch.float64, device=a.device)
+    L = nat.lib()
+    nat.check(L.hp_reduction_components(ctypes.c_void_p(iset.handle), ctypes.c_void_p(full.handle),
+                                        nat.HP_C128 if a.is_complex() else nat.HP_F64, ctypes.c_void_p(a.data_ptr()),
+                                        ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(comp.data_ptr()),
+                                        nat.stream_ptr()))
+    comp = iset._from_canon(comp)
+    return ErrorReport(iset, comp.cpu().numpy() if host else comp,
+                       _metadata(iset, approx, MEASURE_REDUCTION, full_size=full.size))
+
+
+def reduction_local_mask(iset: IndexSet, approx: ChebApprox) -> np.ndarray:
+    """Indices whose reduction error must vanish: j + r in the set for every degree tuple r of
+    the surrogate (error_lab.py:133-148), by device up-walks through the neighbour tables."""
+    import torch
+
+    degs, _ = _term_arrays(approx, iset.dim)
+    mask = torch.empty(iset.size, dtype=torch.uint8, device="cuda")
+    nat.check(nat.lib().hp_reduction_local_mask(ctypes.c_void_p(iset.handle), degs.ctypes.data_as(nat.c_i32p),
+                                                degs.shape[0], ctypes.c_void_p(mask.data_ptr()), nat.stream_ptr()))
+    return iset._from_canon(mask).cpu().numpy().astype(bool)
 
 
 def make_decay_vector(iset: IndexSet, beta: int, *, normalized: bool = True) -> CoeffVector:
@@ -58,7 +146,7 @@ class _HamMatVec:
         fh = self.fh
         iset = fh.iset
         n = iset.size
-        v, host = fh._vec(v0)
+        v, kind = fh._vec(v0)
         if float(torch.linalg.vector_norm(v)) == 0.0:
             raise ValueError("starting vector must be nonzero")
         degs, coeffs = _term_arrays(self.approx, iset.dim)
@@ -78,8 +166,8 @@ class _HamMatVec:
                                ctypes.c_void_p(ws.data_ptr()), ws.numel(), nat.stream_ptr()))
         d = diag.cpu().numpy()
         m = int(d[0])
-        basis = V[:m].T
-        return LanczosFactorization(basis.cpu().numpy() if host else basis, al[:m].cpu().numpy(),
+        basis = fh._out(V[:m], kind).T  # rows in the caller's order, as an (n, m) view
+        return LanczosFactorization(basis, al[:m].cpu().numpy(),
                                     be[:max(m - 1, 0)].cpu().numpy(), None if d[2] < 0 else int(d[2]),
                                     float(d[1]))
 
@@ -104,14 +192,38 @@ class FastHamiltonian:
 
     # -- device stepping ---------------------------------------------------------
     def _vec(self, y):
+        """The state as a fresh complex128 CUDA tensor in the device set's order, and its kind
+        ("numpy", "cpu" for a host torch tensor, "cuda") for `_out`."""
         import torch
 
         if _is_torch(y):
-            return y.to(device="cuda", dtype=torch.complex128).contiguous().clone(), False
-        arr = np.ascontiguousarray(np.asarray(y), dtype=np.complex128)
-        if arr.shape != (self.iset.size,):
-            raise ValueError(f"state has shape {arr.shape}, expected ({self.iset.size},)")
-        return torch.from_numpy(arr).cuda(), True
+            kind = "cuda" if y.is_cuda else "cpu"
+            t = y.to(device="cuda", dtype=torch.complex128, non_blocking=True).contiguous()
+            if t.data_ptr() == y.data_ptr():
+                t = t.clone()  # the step updates the state in place
+        else:
+            kind = "numpy"
+            arr = np.ascontiguousarray(np.asarray(y), dtype=np.complex128)
+            if arr.shape != (self.iset.size,):
+                raise ValueError(f"state has shape {arr.shape}, expected ({self.iset.size},)")
+            t = torch.from_numpy(arr).cuda()
+        if t.shape[-1] != self.iset.size:
+            raise ValueError(f"state has shape {tuple(t.shape)}, expected ({self.iset.size},)")
+        return self.iset._to_canon(t), kind
+
+    def _out(self, t, kind, *, copy: bool = False):
+        """A device-order tensor back to the caller's form and order: numpy for numpy input, a
+        pinned host tensor for a host tensor, else a CUDA tensor (a copy when ``copy``)."""
+        import torch
+
+        u = self.iset._from_canon(t)
+        if kind == "numpy":
+            return u.cpu().numpy()
+        if kind == "cpu":
+            out = torch.empty(u.shape, dtype=u.dtype, pin_memory=True)
+            out.copy_(u)
+            return out
+        return u.clone() if copy and u is t else u
 
     def _workspace(self, scheme_code, term_lists, m):
         import torch
@@ -149,7 +261,7 @@ class FastHamiltonian:
 
         if want_fac:
             return self._step_with_factorization(approxes, y, h, m, reorth)
-        ydev, host = self._vec(y)
+        ydev, kind = self._vec(y)
         if float(torch.linalg.vector_norm(ydev)) == 0.0:
             raise ValueError("starting vector must be nonzero")
         diag = torch.zeros(4, dtype=torch.float64, device="cuda")
@@ -157,7 +269,7 @@ class FastHamiltonian:
         d = diag.cpu().numpy()
         if d[3] != 0:
             raise RuntimeError("tridiagonal QL failed to converge")
-        return ydev.cpu().numpy() if host else ydev
+        return self._out(ydev, kind)
 
     def _step_with_factorization(self, approxes, y, h, m, reorth):
         """exp(-i h B) y together with the Lanczos factorization it was built from.
@@ -172,9 +284,13 @@ class FastHamiltonian:
 
         from .krylov_propagator import _expm_col_dev, _lanczos_generic
 
-        ydev, host = self._vec(y)
+        # caller-order device vector: the factorization's basis is in the caller's order (every
+        # matvec below permutes at the applier boundary itself)
+        host = not _is_torch(y)
+        yd = torch.from_numpy(np.ascontiguousarray(y, dtype=np.complex128)).cuda() if host else \
+            y.to(device="cuda", dtype=torch.complex128).contiguous()
         if len(approxes) == 1:
-            fac = _HamMatVec(self, approxes[0]).lanczos(ydev, m, reorthogonalize=reorth)
+            fac = _HamMatVec(self, approxes[0]).lanczos(yd, m, reorthogonalize=reorth)
         else:
             a1, a2 = _HamMatVec(self, approxes[0]), _HamMatVec(self, approxes[1])
             gamma = _SQRT3 / 12.0 * h
@@ -183,12 +299,13 @@ class FastHamiltonian:
                 y1, y2 = a1(v), a2(v)
                 return 0.5 * (y1 + y2) - 1j * gamma * (a2(y1) - a1(y2))
 
-            fac = _lanczos_generic(gl2, ydev, m, reorth)
+            fac = _lanczos_generic(gl2, yd, m, reorth)
         col = _expm_col_dev(fac.alpha, fac.beta, h)
-        out = float(torch.linalg.vector_norm(ydev)) * (fac.basis @ col)
-        return (out.cpu().numpy() if host else out), LanczosFactorization(
-            fac.basis.cpu().numpy() if host else fac.basis, fac.alpha, fac.beta, fac.breakdown_at,
-            fac.hermiticity_defect)
+        out = float(torch.linalg.vector_norm(yd)) * (fac.basis @ col)
+        if host:
+            return out.cpu().numpy(), LanczosFactorization(fac.basis.cpu().numpy(), fac.alpha, fac.beta,
+                                                           fac.breakdown_at, fac.hermiticity_defect)
+        return (out if y.is_cuda else out.cpu()), fac
 
     def _approxes(self, scheme: MagnusScheme, t: float, h: float):
         if scheme.name == "midpoint":
@@ -206,7 +323,7 @@ class FastHamiltonian:
         """krylov_propagator.py:247-263 with the state resident on the device."""
         import torch
 
-        ydev, host = self._vec(y0)
+        ydev, kind = self._vec(y0)
         if float(torch.linalg.vector_norm(ydev)) == 0.0:
             raise ValueError("starting vector must be nonzero")
         diag = torch.zeros((nsteps, 4), dtype=torch.float64, device="cuda")
@@ -219,8 +336,8 @@ class FastHamiltonian:
                 # call gets its own array/tensor (the device state is overwritten in place)
                 if float(diag[k, 3]) != 0:
                     raise RuntimeError("tridiagonal QL failed to converge")
-                callback(k + 1, t + h, ydev.cpu().numpy() if host else ydev.clone())
+                callback(k + 1, t + h, self._out(ydev, kind, copy=True))
         if bool((diag[:, 3] != 0).any()):
             raise RuntimeError("tridiagonal QL failed to converge")
         self.last_diagnostics = diag
-        return ydev.cpu().numpy() if host else ydev
+        return self._out(ydev, kind)

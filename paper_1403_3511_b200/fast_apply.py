@@ -101,17 +101,19 @@ class PolynomialApplier:
         import torch
 
         t, host, batch, dtype = _Dev.to_device(w, self.iset.size)
+        t = self.iset._to_canon(t)
         out = torch.empty_like(t)
         nat.check(nat.lib().hp_apply_coordinate(ctypes.c_void_p(self.iset.handle), axis, dtype,
                                                 ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                                 batch, nat.stream_ptr()))
-        return _Dev.back(out, host)
+        return _Dev.back(self.iset._from_canon(out), host)
 
     # -- T_deg(X_axis / L) (fast_apply.py:94-106, 281-302) -------------------------
     def cheb_apply(self, axis: int, degree: int, halfwidth: float, v):
         import torch
 
         t, host, batch, dtype = _Dev.to_device(v, self.iset.size)
+        t = self.iset._to_canon(t)
         out = torch.empty_like(t)
         L = nat.lib()
         h = ctypes.c_void_p(self.iset.handle)
@@ -119,7 +121,7 @@ class PolynomialApplier:
         nat.check(L.hp_cheb_apply(h, axis, int(degree), float(halfwidth), dtype, ctypes.c_void_p(t.data_ptr()),
                                   ctypes.c_void_p(out.data_ptr()), batch, ctypes.c_void_p(ws.data_ptr()),
                                   ws.numel(), nat.stream_ptr()))
-        return _Dev.back(out, host)
+        return _Dev.back(self.iset._from_canon(out), host)
 
     def _chebyshev_axis(self, axis, deg, halfwidth, wm, wp, sp, tmp):
         """Padded-buffer form used by the reference's cheb_of_coordinate_apply."""
@@ -142,6 +144,7 @@ class PolynomialApplier:
             order_arr = np.ascontiguousarray(order, dtype=np.int32)
         degs, coeffs = _term_arrays(approx, N)
         t, host, batch, dtype = _Dev.to_device(v, self.iset.size)
+        t = self.iset._to_canon(t)
         out = torch.empty_like(t)
         L = nat.lib()
         h = ctypes.c_void_p(self.iset.handle)
@@ -152,7 +155,7 @@ class PolynomialApplier:
             ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(out.data_ptr()), batch, flags,
             order_arr.ctypes.data_as(nat.c_i32p) if order_arr is not None else None,
             ctypes.c_void_p(ws.data_ptr()), ws.numel(), nat.stream_ptr()))
-        return _Dev.back(out, host)
+        return _Dev.back(self.iset._from_canon(out), host)
 
     def _into_entry(self, approx, x, flags: int, batch: int):
         """Term arrays of `approx` and a workspace for the device-resident entry points.
@@ -195,8 +198,9 @@ class PolynomialApplier:
         so a repeated call is a single C-ABI launch sequence with no host
         allocation (bench.py's timed step).
         """
-        import torch
-
+        if self.iset.permuted:  # explicit unsorted index list: permute at the boundary
+            y.copy_(self._poly(approx, x, flags, None))
+            return
         batch = 1 if x.dim() == 1 else x.shape[0]
         _, degs, coeffs, h, batch, dtype, ws = self._into_entry(approx, x, flags, batch)
         nat.check(nat.lib().hp_apply_polynomial(
@@ -244,6 +248,9 @@ class PolynomialApplier:
             raise ValueError("apply_host_into expects two CPU tensors of the same shape and dtype")
         if not (x_host.is_contiguous() and y_host.is_contiguous()):
             raise ValueError("apply_host_into expects contiguous tensors")
+        if self.iset.permuted:
+            y_host.copy_(self._poly(approx, x_host.cuda(), flags, None).cpu())
+            return
         batch = 1 if x_host.dim() == 1 else x_host.shape[0]
         _, degs, coeffs, h, batch, dtype, ws = self._into_entry(approx, x_host, flags, batch)
         # device staging buffers, shared like the workspace (per shape, dtype and stream)
@@ -276,10 +283,11 @@ class PolynomialApplier:
         import torch
 
         t, host, batch, dtype = _Dev.to_device(v, self.iset.size)
+        t = self.iset._to_canon(t)
         out = torch.empty_like(t)
         nat.check(nat.lib().hp_square_sum(ctypes.c_void_p(self.iset.handle), dtype, ctypes.c_void_p(t.data_ptr()),
                                           ctypes.c_void_p(out.data_ptr()), batch, nat.stream_ptr()))
-        return _Dev.back(out, host)
+        return _Dev.back(self.iset._from_canon(out), host)
 
 
 def get_applier(iset: IndexSet) -> PolynomialApplier:
