@@ -53,7 +53,8 @@ def check_sketch(gold, key, y, tol=TOL):
     samp = gold[key + "_samp"]
     assert rel_l2(y[:head.shape[0]], head) <= tol
     assert rel_l2(y[::step], samp) <= tol
-    assert abs(float(np.linalg.norm(y)) / float(gold[key + "_norm"]) - 1.0) <= tol
+    # the 2-norm goes through BLAS, whose summation order follows the host's thread count
+    assert abs(float(np.linalg.norm(y)) / float(gold[key + "_norm"]) - 1.0) <= max(tol, 1e-14)
 
 
 def _need(gold, key):
