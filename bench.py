@@ -292,10 +292,13 @@ def gpu_arm(args, rank, world, local_rank):
         return
 
     sharding = None
-    if (world > 1 or args.force_shard) and w.kind == "full" and w.batch == 1:
+    emu = None  # --shard-geometry R/P: rank R's slab of a P-rank run, measured alone on this GPU
+    if args.shard_geometry:
+        emu = tuple(int(x) for x in args.shard_geometry.split("/"))
+    if (world > 1 or args.force_shard or emu) and w.kind == "full" and w.batch == 1:
         from paper_1403_3511_b200 import sharding as SH
 
-        sharding = SH.SlabShard(w.dim, w.bound, rank, world, halo=w.degree)
+        sharding = SH.SlabShard(w.dim, w.bound, *(emu or (rank, world)), halo=w.degree)
         s = sharding.set
     else:
         s = build_set(hp, w)
@@ -322,7 +325,8 @@ def gpu_arm(args, rank, world, local_rank):
 
     def step_dev():
         if sharding is not None:
-            sharding.apply_polynomial(appl, ap, x, y)
+            # emulated geometry: no peers, the seeded halo planes stand in for the exchanged ones
+            sharding.apply_polynomial(appl, ap, x, y, exchange=(lambda g, b: None) if emu else None)
         else:
             appl.apply_into(ap, x, y)
 
@@ -366,7 +370,9 @@ def gpu_arm(args, rank, world, local_rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_max = float(t)
     ms_step = ms_max / args.steps
-    if sharding is not None:
+    if emu:
+        total_coeffs = (sharding.geo.hi - sharding.geo.lo) * sharding.geo.plane  # this rank's planes
+    elif sharding is not None:
         total_coeffs = sharding.global_size
     elif part:
         total_coeffs = n_local * w.batch  # all ranks' vectors
@@ -440,12 +446,12 @@ def gpu_arm(args, rank, world, local_rank):
     # the named propagation run of the workload (cfg4: 50 midpoint steps at dt = 0.005), timed in
     # the same process after the matvec buffers are released
     prop = None
-    if w.nsteps > 0 and not args.no_prop:
+    if w.nsteps > 0 and not args.no_prop and not emu:
         del x, y
         if not args.no_e2e:
             del xh, yh
         torch.cuda.empty_cache()
-        prop = propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind, sharding is not None)
+        prop = propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind, sharding is not None and world > 1)
 
     if rank == 0:
         line = {"metric": "Galerkin matvec throughput", "value": value, "unit": "coeffs/s", "n_gpus": world,
@@ -457,7 +463,9 @@ def gpu_arm(args, rank, world, local_rank):
                            "batch": w.batch, "nterms": int(ap.nterms), "halfwidth": W.HALFWIDTH,
                            "l2": "L2 flushed between steps (256 MB write outside the per-step events)" if flush_l2
                            else "inputs larger than L2 (no flush)",
-                           "parallelism": f"slab-j1 x{world}" if sharding is not None else
+                           "parallelism": (f"slab-j1 rank {emu[0]} of {emu[1]} (emulated on one GPU: exchange "
+                                           f"skipped, {sharding.schedule()} schedule; value = that rank's planes/s)")
+                           if emu else f"slab-j1 x{world}" if sharding is not None else
                            ("single" if world == 1 else f"batch/{world}" if part else f"replicas x{world}")},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "propagation": prop}
@@ -627,6 +635,8 @@ def main():
     ap.add_argument("--no-prop", action="store_true", help="skip the propagation leg")
     ap.add_argument("--prop-steps", type=int, default=10,
                     help="Magnus steps timed in the propagation leg (capped at the named run's step count)")
+    ap.add_argument("--shard-geometry", default=None, metavar="R/P",
+                    help="time rank R's slab matvec of a P-rank cfg4 run alone on one GPU (no exchange)")
     ap.add_argument("--force-shard", action="store_true",
                     help="run the slab-sharded code path even at one rank (tests the N>1 path's local part)")
     args = ap.parse_args()

@@ -147,25 +147,44 @@ class SlabShard:
         ihi = hi - (RADIUS if g.rank < g.world - 1 else 0)
         return (ilo, ihi) if ihi > ilo else None
 
+    def schedule(self) -> str:
+        """"overlap": interior planes while the halo is in flight, then the two boundary ranges;
+        "single": exchange, then ONE launch over the owned planes.
+
+        Every plane-range launch of the fused kernel re-reads RADIUS warm-up planes on each side,
+        so the overlapped schedule reads owned + 24 planes (interior: owned; each boundary range:
+        its 4 planes + 8) against owned + 8 for the single launch, which in turn exposes the
+        exchange (2 x RADIUS planes over NVLink, ~1/10 of a plane's HBM time per plane at 900 GB/s
+        vs 6.5 TB/s x 0.55).  With few owned planes the re-reads dominate: single launch for
+        <= 32 owned planes (4+ ranks on a 128-plane cube), overlap above.
+        """
+        import os
+
+        forced = os.environ.get("HP_SLAB_SCHEDULE")
+        if forced in ("single", "overlap"):
+            return forced
+        g = self.geo
+        return "single" if g.world > 1 and (g.hi - g.lo) <= 32 else "overlap"
+
     def apply_polynomial(self, appl, ap, x, y, flags: int = 0, overlap: bool = True, exchange=None, dot=None):
         """y[own] = W(X) x on this rank's planes; x, y are box-sized device tensors.
 
-        With `overlap`, the halo exchange runs on a side stream while the interior planes are
-        computed (hp_apply_polynomial_planes), then the boundary planes; otherwise exchange,
-        then one matvec over the box.  `exchange(geo, x)` replaces halo_exchange (tests).
-        `dot` (a float64 device tensor of 2): the owned rows of x^H y are added to it by the
-        fused kernel when the surrogate is in its class; returns whether it was.
+        With `overlap` and the "overlap" schedule, the halo exchange runs on a side stream while
+        the interior planes are computed (hp_apply_polynomial_planes), then the boundary planes;
+        otherwise exchange, then one launch over the owned planes.  `exchange(geo, x)` replaces
+        halo_exchange (tests).  `dot` (a float64 device tensor of 2): the owned rows of x^H y are
+        added to it by the fused kernel when the surrogate is in its class; returns whether it was.
         """
         import torch
 
         exch = exchange or halo_exchange
         g = self.geo
         lo, hi = g.lo - g.blo, g.hi - g.blo
-        rng = self.interior() if overlap and g.world > 1 else None
+        rng = self.interior() if overlap and g.world > 1 and self.schedule() == "overlap" else None
         if rng is None or not appl.apply_planes_into(ap, x, y, rng[0], rng[0], flags):
             exch(g, x)
-            if dot is not None and appl.apply_planes_into(ap, x, y, lo, hi, flags, dot=dot):
-                return True
+            if appl.apply_planes_into(ap, x, y, lo, hi, flags, dot=dot):  # one launch, owned planes
+                return dot is not None
             appl.apply_into(ap, x, y, flags)
             return False
         main = torch.cuda.current_stream()
