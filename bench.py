@@ -451,7 +451,8 @@ def gpu_arm(args, rank, world, local_rank):
         if not args.no_e2e:
             del xh, yh
         torch.cuda.empty_cache()
-        prop = propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind, sharding is not None and world > 1)
+        prop = propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind,
+                               sharding is not None and torch.distributed.is_initialized())
 
     if rank == 0:
         line = {"metric": "Galerkin matvec throughput", "value": value, "unit": "coeffs/s", "n_gpus": world,
@@ -604,7 +605,10 @@ def step_mode(args, w, rank, world, local_rank, hbm, peak_kind):
     if w.nsteps == 0:
         raise SystemExit(f"{w.name} has no propagation run (cfg1, cfg3, cfg4 have)")
     args.prop_steps = w.nsteps if args.steps == 20 else args.steps
-    sharded = (world > 1 or args.force_shard) and w.kind == "full" and w.batch == 1
+    import torch
+
+    sharded = (world > 1 or args.force_shard) and w.kind == "full" and w.batch == 1 and \
+        torch.distributed.is_initialized()
     p = propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind, sharded)
     if rank != 0:
         return
@@ -648,7 +652,10 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank)
         return
-    if world > 1:
+    # a process group also for --force-shard under torchrun at one rank (the sharded code path,
+    # collectives included, measured on one GPU)
+    dist_on = world > 1 or (args.force_shard and "MASTER_ADDR" in os.environ)
+    if dist_on:
         import torch
 
         torch.cuda.set_device(local_rank)
@@ -656,7 +663,7 @@ def main():
     try:
         gpu_arm(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if dist_on:
             import torch
 
             torch.distributed.barrier()

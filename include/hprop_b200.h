@@ -158,9 +158,39 @@ hp_status hp_apply_polynomial_planes_dot(hp_set_t s, const int32_t* degrees_host
                                          void* out_dev, int plane_lo, int plane_hi, int flags, double* dot_dev,
                                          void* workspace_dev, size_t workspace_bytes, void* stream);
 
+/* The same with the harmonic confinement q * sum_l x_l^2 (fast_apply.py:229-245, error_lab.py:176-183)
+ * folded into the fused kernel's single-axis bands, so A(t) v of a harmonic_part != 0 potential stays
+ * one launch with its in-kernel dot (slab-sharded propagation). */
+hp_status hp_apply_hamiltonian_planes_dot(hp_set_t s, const int32_t* degrees_host, const double* coeffs_host,
+                                          int nterms, double halfwidth, double q, int dtype, const void* in_dev,
+                                          void* out_dev, int plane_lo, int plane_hi, int flags, double* dot_dev,
+                                          void* workspace_dev, size_t workspace_bytes, void* stream);
+
 /* apply_square_sum -- fast_apply.py:202-245 (exact restricted sum_l x_l^2) */
 hp_status hp_square_sum(hp_set_t s, int dtype, const void* in_dev, void* out_dev,
                         int64_t batch, void* stream);
+
+/* ---- Lanczos scalars on the device for distributed callers ------------------------
+ * The slab-sharded propagation (sharding.sharded_propagate) runs the scaled Lanczos recurrence of
+ * krylov_propagator.py:58-104 with every scalar -- alpha_k, beta_k, the basis scales, breakdown
+ * (beta <= tol truncates m, :90-93), the QL + exp column (:107-186) -- in an opaque device state,
+ * so no iteration waits on the host; cross-rank sums of the per-rank partials are formed by the
+ * caller (NCCL all-gather + rank-ordered sum) and handed in as device (re, im) pairs. */
+size_t hp_lz_state_bytes(void);
+hp_status hp_lz_init(void* state_dev, int m, void* stream);
+/* what: 1 = ||y||^2 (sets nrm0, scale_0), 6 = u_k^H A u_k (alpha_k = scale_k^2 re), 7 = ||w_{k+1}||^2
+ * (beta_k, scale_{k+1}, or breakdown) */
+hp_status hp_lz_set(void* state_dev, int k, int what, const double* value_dev, double tol, void* stream);
+/* w_{k+1} = s_k z - alpha_k s_k w_k - beta_{k-1} s_{k-1} w_{k-1} with this rank's ||w_{k+1}||^2
+ * partial written to nrm2_out_dev[0]; a no-op past a breakdown.  ws: hp_reduce_workspace_bytes */
+hp_status hp_lz_update(int64_t n, const void* z_dev, const void* wk_dev, const void* wkm1_dev, void* wn_dev,
+                       const void* state_dev, int k, double* nrm2_out_dev, void* ws, void* stream);
+hp_status hp_lz_expm(void* state_dev, double tau, void* stream);
+/* out = nrm0 sum_{k < m_eff} col_k s_k w_k over m basis pointers (out may alias vecs[0]) */
+hp_status hp_lz_combine(int64_t n, int m, const void* const* vecs_host, const void* state_dev, void* out_dev,
+                        void* stream);
+/* diag = {m_eff, hermiticity defect, breakdown_at (-1), QL failure}; alpha/beta may be null */
+hp_status hp_lz_diag(const void* state_dev, double* diag_dev, double* alpha_dev, double* beta_dev, void* stream);
 
 /* ---- full cube <-> subset maps (index_set.py:296-319, error_lab.py:114-148) ---- */
 

@@ -60,7 +60,16 @@ SIGNATURES = {
                                            c_int, c_vp, c_sz, c_vp]),
     "hp_apply_polynomial_planes_dot": (c_int, [c_vp, c_i32p, c_dblp, c_int, c_dbl, c_int, c_vp, c_vp, c_int, c_int,
                                                c_int, c_vp, c_vp, c_sz, c_vp]),
+    "hp_apply_hamiltonian_planes_dot": (c_int, [c_vp, c_i32p, c_dblp, c_int, c_dbl, c_dbl, c_int, c_vp, c_vp, c_int,
+                                                c_int, c_int, c_vp, c_vp, c_sz, c_vp]),
     "hp_square_sum": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_vp]),
+    "hp_lz_state_bytes": (c_sz, []),
+    "hp_lz_init": (c_int, [c_vp, c_int, c_vp]),
+    "hp_lz_set": (c_int, [c_vp, c_int, c_int, c_vp, c_dbl, c_vp]),
+    "hp_lz_update": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp]),
+    "hp_lz_expm": (c_int, [c_vp, c_dbl, c_vp]),
+    "hp_lz_combine": (c_int, [c_i64, c_int, c_vp, c_vp, c_vp, c_vp]),
+    "hp_lz_diag": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "hp_restrict": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_i64, c_vp]),
     "hp_extend": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_i64, c_vp]),
     "hp_reduction_components": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),

@@ -721,6 +721,14 @@ hp_status hp_apply_polynomial_planes_dot(hp_set_t s, const int32_t* degrees, con
                                          double halfwidth, int dtype, const void* in, void* out, int plane_lo,
                                          int plane_hi, int flags, double* dot_dev, void* ws, size_t ws_bytes,
                                          void* stream) {
+  return hp_apply_hamiltonian_planes_dot(s, degrees, coeffs, nterms, halfwidth, 0.0, dtype, in, out, plane_lo,
+                                         plane_hi, flags, dot_dev, ws, ws_bytes, stream);
+}
+
+hp_status hp_apply_hamiltonian_planes_dot(hp_set_t s, const int32_t* degrees, const double* coeffs, int nterms,
+                                          double halfwidth, double q, int dtype, const void* in, void* out,
+                                          int plane_lo, int plane_hi, int flags, double* dot_dev, void* ws,
+                                          size_t ws_bytes, void* stream) {
   hp_status rc = check_set(s);
   if (rc) return rc;
   if ((rc = check_terms(s, degrees, nterms, halfwidth))) return rc;
@@ -733,7 +741,7 @@ hp_status hp_apply_polynomial_planes_dot(hp_set_t s, const int32_t* degrees, con
   auto terms = make_terms(s->dim, degrees, coeffs, nterms);
   bool done = false;
   rc = fullgrid_apply_planes(s, terms, halfwidth, dtype, in, out, plane_lo, plane_hi, flags, ws, ws_bytes,
-                             as_stream(stream), &done, dot_dev);
+                             as_stream(stream), &done, dot_dev, q);
   if (rc) return rc;
   if (!done) return fail(HP_ERR_VALUE, "plane-range matvec: the fused full-cube evaluator only");
   return HP_OK;

@@ -573,7 +573,7 @@ __global__ void k_fg_dot_accum(const double2* __restrict__ partial, int n, doubl
 
 hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                                 const void* in, void* out, int plo, int phi, int flags, void* ws, size_t ws_bytes,
-                                cudaStream_t st, bool* done, double* dot_accum) {
+                                cudaStream_t st, bool* done, double* dot_accum, double sq) {
   *done = false;
   FgPlan F = classify(s, terms, dtype, 1, flags);
   if (!F.ok || !fg_single_class(F)) return HP_OK;
@@ -582,7 +582,7 @@ hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& term
     return HP_OK;
   }
   bool ok = false;
-  hp_status rc = fg_prepare(s, terms, halfwidth, dtype, 1, flags, ws, ws_bytes, st, &F, &ok);
+  hp_status rc = fg_prepare(s, terms, halfwidth, dtype, 1, flags, ws, ws_bytes, st, &F, &ok, sq);
   if (rc || !ok) return rc;
   const double* P = (const double*)ws;
   const double* G = P + 4 * FG_MAXN * FG_W;

@@ -84,10 +84,23 @@ __device__ double2 block_sum_partials(const double2* partial, int np) {
 
 // what: 1 nrm0 and scale_0 (norm), 4 write dot to out[0..1], 5 write norm to out[0],
 //       6 alpha_k (scaled dot), 7 beta_k / scale_{k+1} / breakdown (norm), 8 reorth coefficient
+__device__ void lz_scalar(double2 s, LzState* st, int k, int what, double tol, double* out);
+
 __global__ void __launch_bounds__(HP_RED_THREADS) k_red_final(const double2* partial, int np, LzState* st,
                                                               int k, int what, double tol, double* out) {
   double2 s = block_sum_partials(partial, np);
   if (threadIdx.x != 0) return;
+  lz_scalar(s, st, k, what, tol, out);
+}
+
+// one already-reduced scalar into the Lanczos state (the sharded path: the per-rank partials are
+// summed across ranks in rank order before this)
+__global__ void k_lz_set(const double* value, LzState* st, int k, int what, double tol) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  lz_scalar(make_double2(value[0], value[1]), st, k, what, tol, nullptr);
+}
+
+__device__ void lz_scalar(double2 s, LzState* st, int k, int what, double tol, double* out) {
   if (what == 4) { out[0] = s.x; out[1] = s.y; return; }
   if (what == 5) { out[0] = sqrt(s.x); return; }
   if (st->broken && k >= st->m_eff) return;
@@ -201,6 +214,26 @@ __global__ void k_lz_combine_s(int64_t n, const double2* w0, const double2* __re
     double2 acc = make_double2(0.0, 0.0);
     for (int k = 0; k < m; ++k) {
       double2 v = (k == 0 ? w0 : V + (int64_t)(k - 1) * n)[i];
+      acc.x += v.x * c[k].x - v.y * c[k].y;
+      acc.y += v.x * c[k].y + v.y * c[k].x;
+    }
+    y[i] = make_double2(s * acc.x, s * acc.y);
+  }
+}
+
+// the same combine over separate basis vectors (the sharded path's per-rank own-plane views)
+struct LzPtrs {
+  const double2* v[HP_MAXM];
+};
+__global__ void k_lz_combine_ptrs(int64_t n, LzPtrs P, const LzState* st, double2* y) {
+  const int m = st->m_eff;
+  const double s = st->nrm0;
+  double2 c[HP_MAXM];
+  for (int k = 0; k < m; ++k) c[k] = make_double2(st->col[k].x * st->scale[k], st->col[k].y * st->scale[k]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < m; ++k) {
+      double2 v = P.v[k][i];
       acc.x += v.x * c[k].x - v.y * c[k].y;
       acc.y += v.x * c[k].y + v.y * c[k].x;
     }
@@ -724,6 +757,65 @@ hp_status hp_cdot(int64_t n, const void* a, const void* b, double* out, void* ws
 hp_status hp_cnrm2(int64_t n, const void* a, double* out, void* ws, void* stream) {
   cudaStream_t st = as_stream(stream);
   return reduce(1, n, (const double2*)a, nullptr, (double2*)ws, nullptr, 0, 5, 0.0, out, st);
+}
+
+// ---- device-resident Lanczos scalars for distributed callers (sharding.sharded_propagate)
+
+size_t hp_lz_state_bytes(void) { return sizeof(LzState); }
+
+hp_status hp_lz_init(void* state_dev, int m, void* stream) {
+  hp_status rc = check_m(m);
+  if (rc) return rc;
+  k_lz_init<<<1, 32, 0, as_stream(stream)>>>((LzState*)state_dev, m);
+  HP_LAUNCH_CHECK("k_lz_init");
+  return HP_OK;
+}
+
+hp_status hp_lz_set(void* state_dev, int k, int what, const double* value_dev, double tol, void* stream) {
+  if (!state_dev || !value_dev || k < 0 || k >= HP_MAXM) return fail(HP_ERR_VALUE, "lz_set: bad arguments");
+  if (what != 1 && what != 6 && what != 7) return fail(HP_ERR_VALUE, "lz_set: what must be 1, 6 or 7");
+  k_lz_set<<<1, 32, 0, as_stream(stream)>>>(value_dev, (LzState*)state_dev, k, what, tol);
+  HP_LAUNCH_CHECK("k_lz_set");
+  return HP_OK;
+}
+
+hp_status hp_lz_update(int64_t n, const void* z, const void* wk, const void* wkm1, void* wn, const void* state_dev,
+                       int k, double* nrm2_out_dev, void* ws, void* stream) {
+  if (n < 0 || !z || !wk || !wn || !state_dev || !nrm2_out_dev || !ws || (k > 0 && !wkm1))
+    return fail(HP_ERR_VALUE, "lz_update: null buffer");
+  cudaStream_t st = as_stream(stream);
+  k_lz_update_s<<<HP_RED_BLOCKS, HP_RED_THREADS, 0, st>>>(n, (const double2*)z, (const double2*)wk,
+                                                           (const double2*)wkm1, (double2*)wn,
+                                                           (const LzState*)state_dev, k, (double2*)ws);
+  HP_LAUNCH_CHECK("k_lz_update_s");
+  k_red_final<<<1, HP_RED_THREADS, 0, st>>>((double2*)ws, HP_RED_BLOCKS, nullptr, 0, 4, 0.0, nrm2_out_dev);
+  HP_LAUNCH_CHECK("k_red_final");
+  return HP_OK;
+}
+
+hp_status hp_lz_expm(void* state_dev, double tau, void* stream) {
+  k_lz_expm<<<1, 32, 0, as_stream(stream)>>>((LzState*)state_dev, tau);
+  HP_LAUNCH_CHECK("k_lz_expm");
+  return HP_OK;
+}
+
+hp_status hp_lz_combine(int64_t n, int m, const void* const* vecs_host, const void* state_dev, void* out,
+                        void* stream) {
+  hp_status rc = check_m(m);
+  if (rc) return rc;
+  if (!vecs_host || !state_dev || !out) return fail(HP_ERR_VALUE, "lz_combine: null buffer");
+  LzPtrs P{};
+  for (int k = 0; k < m; ++k) P.v[k] = (const double2*)vecs_host[k];
+  k_lz_combine_ptrs<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, P, (const LzState*)state_dev,
+                                                                     (double2*)out);
+  HP_LAUNCH_CHECK("k_lz_combine_ptrs");
+  return HP_OK;
+}
+
+hp_status hp_lz_diag(const void* state_dev, double* diag_dev, double* alpha_dev, double* beta_dev, void* stream) {
+  k_lz_diag<<<1, 32, 0, as_stream(stream)>>>((const LzState*)state_dev, diag_dev, alpha_dev, beta_dev);
+  HP_LAUNCH_CHECK("k_lz_diag");
+  return HP_OK;
 }
 
 hp_status hp_expm_tridiag_column(const double* alpha, const double* beta, int m, double tau, void* col,

@@ -79,7 +79,7 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
 
 hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                                 const void* in, void* out, int plo, int phi, int flags, void* ws, size_t ws_bytes,
-                                cudaStream_t st, bool* done, double* dot_accum = nullptr);
+                                cudaStream_t st, bool* done, double* dot_accum = nullptr, double sq = 0.0);
 // per-device host<->device copy streams of the streamed entry points (hp_fullgrid.cu)
 hp_status copy_streams(cudaStream_t* in, cudaStream_t* out);
 hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,

@@ -208,12 +208,15 @@ class PolynomialApplier:
             float(approx.halfwidth), dtype, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), batch,
             flags, None, ctypes.c_void_p(ws.data_ptr()), ws.numel(), nat.stream_ptr()))
 
-    def apply_planes_into(self, approx, x, y, plane_lo: int, plane_hi: int, flags: int = 0, dot=None) -> bool:
-        """y <- W(X) x on the output j1-planes [plane_lo, plane_hi) of a full cube / slab only.
+    def apply_planes_into(self, approx, x, y, plane_lo: int, plane_hi: int, flags: int = 0, dot=None,
+                          q: float = 0.0) -> bool:
+        """y <- W(X) x [+ q sum_l x_l^2 x] on the output j1-planes [plane_lo, plane_hi) of a full
+        cube / slab only.
 
-        Reads input planes plane_lo - 4 .. plane_hi + 3 (hp_apply_polynomial_planes).  Returns
-        False (nothing launched) when the surrogate is outside the fused full-cube class; the
-        answer is cached per term structure (degrees and nonzero pattern), shape and flags.
+        Reads input planes plane_lo - 4 .. plane_hi + 3 (hp_apply_hamiltonian_planes_dot; q folds
+        the exact square sum into the same launch).  Returns False (nothing launched) when the
+        surrogate is outside the fused full-cube class; the answer is cached per term structure
+        (degrees and nonzero pattern), shape and flags.
         """
         _, degs, coeffs, h, _batch, dtype, ws = self._into_entry(approx, x, flags, 1)
         key = (degs.tobytes(), (np.asarray(coeffs) != 0).tobytes(), tuple(x.shape), x.dtype, flags)
@@ -222,9 +225,9 @@ class PolynomialApplier:
             return False
         # dot: a float64 device tensor of 2; (re, im) of the in-kernel rows of x^H y over the
         # output planes are ADDED to it (hp_apply_polynomial_planes_dot)
-        st = nat.lib().hp_apply_polynomial_planes_dot(
+        st = nat.lib().hp_apply_hamiltonian_planes_dot(
             h, degs.ctypes.data_as(nat.c_i32p), coeffs.ctypes.data_as(nat.c_dblp), degs.shape[0],
-            float(approx.halfwidth), dtype, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+            float(approx.halfwidth), float(q), dtype, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
             int(plane_lo), int(plane_hi), flags, ctypes.c_void_p(dot.data_ptr()) if dot is not None else None,
             ctypes.c_void_p(ws.data_ptr()), ws.numel(), nat.stream_ptr())
         if st == nat.HP_ERR_VALUE and "fused full-cube" in nat.last_error():

@@ -166,7 +166,8 @@ class SlabShard:
         g = self.geo
         return "single" if g.world > 1 and (g.hi - g.lo) <= 32 else "overlap"
 
-    def apply_polynomial(self, appl, ap, x, y, flags: int = 0, overlap: bool = True, exchange=None, dot=None):
+    def apply_polynomial(self, appl, ap, x, y, flags: int = 0, overlap: bool = True, exchange=None, dot=None,
+                         q: float = 0.0):
         """y[own] = W(X) x on this rank's planes; x, y are box-sized device tensors.
 
         With `overlap` and the "overlap" schedule, the halo exchange runs on a side stream while
@@ -183,21 +184,23 @@ class SlabShard:
         rng = self.interior() if overlap and g.world > 1 and self.schedule() == "overlap" else None
         if rng is None or not appl.apply_planes_into(ap, x, y, rng[0], rng[0], flags):
             exch(g, x)
-            if appl.apply_planes_into(ap, x, y, lo, hi, flags, dot=dot):  # one launch, owned planes
+            if appl.apply_planes_into(ap, x, y, lo, hi, flags, dot=dot, q=q):  # one launch, owned planes
                 return dot is not None
-            appl.apply_into(ap, x, y, flags)
+            appl.apply_into(ap, x, y, flags)  # outside the fused class: whole box, square sum apart
+            if q != 0.0:
+                y.add_(appl.apply_square_sum(x), alpha=q)
             return False
         main = torch.cuda.current_stream()
         side = self.__dict__.setdefault("_side", torch.cuda.Stream())
         side.wait_stream(main)
         with torch.cuda.stream(side):
             exch(g, x)  # NCCL on the side stream
-        appl.apply_planes_into(ap, x, y, rng[0], rng[1], flags, dot=dot)  # reads owned planes only
+        appl.apply_planes_into(ap, x, y, rng[0], rng[1], flags, dot=dot, q=q)  # reads owned planes only
         main.wait_stream(side)
         if rng[0] > lo:
-            appl.apply_planes_into(ap, x, y, lo, rng[0], flags, dot=dot)
+            appl.apply_planes_into(ap, x, y, lo, rng[0], flags, dot=dot, q=q)
         if hi > rng[1]:
-            appl.apply_planes_into(ap, x, y, rng[1], hi, flags, dot=dot)
+            appl.apply_planes_into(ap, x, y, rng[1], hi, flags, dot=dot, q=q)
         return dot is not None
 
     def apply_host(self, appl, ap, x_host, y_host, flags: int = 0) -> None:
@@ -226,6 +229,57 @@ def local_sum(partials):
     for p in partials[1:]:
         total += p
     return total
+
+
+class HostLanczosScalars:
+    """The hp_lz_* state machine on the host (the same scaled recurrence as k_red_final /
+    k_lz_update_s / k_lz_combine_s), for step-op implementations that keep their vectors off the
+    device (the gloo orchestration tests).  Mixed into a class providing ``update`` (host
+    coefficients), ``combine`` and ``expm_col``."""
+
+    def lz_new(self, m):
+        return {"m": m, "m_eff": m, "broken": False, "alpha": [0.0] * m, "beta": [0.0] * m,
+                "scale": [0.0] * (m + 1), "nrm0": 0.0, "col": None}
+
+    def lz_set(self, st, k, what, value, tol):
+        v = float(value[0])
+        if what == "begin":
+            st["nrm0"] = v ** 0.5
+            st["scale"][0] = 1.0 / st["nrm0"]
+            return
+        if st["broken"] and k >= st["m_eff"]:
+            return
+        if what == "alpha":
+            st["alpha"][k] = st["scale"][k] ** 2 * v
+        else:
+            bk = v ** 0.5
+            if bk <= tol:
+                st["broken"], st["m_eff"] = True, k + 1
+            else:
+                st["beta"][k], st["scale"][k + 1] = bk, 1.0 / bk
+
+    def lz_update(self, st, k, w, u, prev, out):
+        import torch
+
+        if st["broken"] and k >= st["m_eff"]:
+            return [torch.zeros(2, dtype=torch.float64) for _ in w]
+        sk = st["scale"][k]
+        cp = -st["beta"][k - 1] * st["scale"][k - 1] if k > 0 else 0.0
+        return self.update(sk, w, -st["alpha"][k] * sk, u, cp, prev, out)
+
+    def lz_finish(self, st, h):
+        me = st["m_eff"]
+        st["col"] = self.expm_col(st["alpha"][:me], st["beta"][:me - 1], h)
+
+    def lz_combine(self, st, U, out):
+        me = st["m_eff"]
+        self.combine(U[:me], np.array([complex(st["col"][k]) * st["scale"][k] * st["nrm0"] for k in range(me)]),
+                     out)
+
+    def lz_diag(self, st):
+        import torch
+
+        return torch.tensor([st["m_eff"], 0.0, -1.0, 0.0], dtype=torch.float64)
 
 
 class DeviceStepOps:
@@ -261,32 +315,31 @@ class DeviceStepOps:
     def matvec(self, ap, boxes):
         """A(t) u on the owned planes of every shard (views into the output boxes); `boxes` are
         box-sized vectors (owned planes valid) whose halos the exchange fills.  Returns (w, dots):
-        dots[i] = this shard's rows of u^H A u formed inside the fused kernel, or None when the
-        surrogate is outside its class (or a square-sum term is added outside it)."""
+        dots[i] = this shard's rows of u^H A u formed inside the fused kernel (the harmonic part q
+        folded into the same launch), or None when the surrogate is outside its class."""
         import torch
 
         nat = self.nat
         ns = len(self.shards)
-        dots = [torch.zeros(2, dtype=torch.float64, device="cuda") for _ in range(ns)] if self.q == 0.0 else None
+        dots = [torch.zeros(2, dtype=torch.float64, device="cuda") for _ in range(ns)]
         got = [False] * ns
         if self.exchange is None:
             for i, sh in enumerate(self.shards):
-                got[i] = sh.apply_polynomial(self.appls[i], ap, boxes[i], self.outs[i], nat.HP_ADD_OSC,
-                                             dot=dots[i] if dots else None)
+                got[i] = sh.apply_polynomial(self.appls[i], ap, boxes[i], self.outs[i], nat.HP_ADD_OSC, dot=dots[i],
+                                             q=self.q)
         else:  # emulated ranks: one exchange over all boxes, then the local matvecs
             self.exchange([sh.geo for sh in self.shards], boxes)
             for i, sh in enumerate(self.shards):
                 g = sh.geo
-                if dots is not None and self.appls[i].apply_planes_into(ap, boxes[i], self.outs[i], g.lo - g.blo,
-                                                                        g.hi - g.blo, nat.HP_ADD_OSC, dot=dots[i]):
+                if self.appls[i].apply_planes_into(ap, boxes[i], self.outs[i], g.lo - g.blo, g.hi - g.blo,
+                                                   nat.HP_ADD_OSC, dot=dots[i], q=self.q):
                     got[i] = True
                 else:
                     self.appls[i].apply_into(ap, boxes[i], self.outs[i], nat.HP_ADD_OSC)
+                    if self.q != 0.0:
+                        self.outs[i].add_(self.appls[i].apply_square_sum(boxes[i]), alpha=self.q)
         w = [self.outs[i][self.own[i]] for i in range(ns)]
-        if self.q != 0.0:
-            for i in range(ns):
-                w[i].add_(self.appls[i].apply_square_sum(boxes[i])[self.own[i]], alpha=self.q)
-        return w, (dots if dots is not None and all(got) else None)
+        return w, (dots if all(got) else None)
 
     def cdot(self, a, b):
         """per shard: a^H b as a float64 (re, im) tensor (fixed summation order)"""
@@ -331,10 +384,57 @@ class DeviceStepOps:
                                              c.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(out[i].data_ptr()),
                                              self.nat.stream_ptr()))
 
-    def expm_col(self, alpha, beta, h):
-        from .krylov_propagator import expm_tridiag_column
+    # -- Lanczos scalars in device memory (hp_lz_*): no host round trip per iteration ---------
+    def lz_new(self, m):
+        import torch
 
-        return expm_tridiag_column(np.array(alpha), np.array(beta), h)
+        st = torch.empty(int(self.L.hp_lz_state_bytes()), dtype=torch.uint8, device="cuda")
+        self.nat.check(self.L.hp_lz_init(self._vp(st), int(m), self.nat.stream_ptr()))
+        return st
+
+    def _vp(self, t):
+        import ctypes
+
+        return ctypes.c_void_p(t.data_ptr())
+
+    def lz_set(self, st, k, what, value, tol):
+        code = {"begin": 1, "alpha": 6, "beta": 7}[what]
+        self.nat.check(self.L.hp_lz_set(self._vp(st), int(k), code, self._vp(value), float(tol), self.nat.stream_ptr()))
+
+    def lz_update(self, st, k, w, u, prev, out):
+        """out = s_k w - alpha_k s_k u - beta_(k-1) s_(k-1) prev per shard (device scalars);
+        per-shard partial ||out||^2 as (x, 0)"""
+        import torch
+
+        parts = []
+        for i in range(len(w)):
+            sc = torch.zeros(2, dtype=torch.float64, device="cuda")
+            self.nat.check(self.L.hp_lz_update(self.nloc[i], self._vp(w[i]), self._vp(u[i]),
+                                               self._vp(prev[i]) if prev is not None else None, self._vp(out[i]),
+                                               self._vp(st), int(k), self._vp(sc), self._vp(self.ws[i]),
+                                               self.nat.stream_ptr()))
+            parts.append(sc)
+        return parts
+
+    def lz_finish(self, st, h):
+        self.nat.check(self.L.hp_lz_expm(self._vp(st), float(h), self.nat.stream_ptr()))
+
+    def lz_combine(self, st, U, out):
+        """out = ||y|| sum_(k < m_eff) col_k s_k U_k per shard (out may alias U_0)"""
+        import ctypes
+
+        mm = len(U)
+        for i in range(len(out)):
+            ptrs = (ctypes.c_void_p * mm)(*[U[k][i].data_ptr() for k in range(mm)])
+            self.nat.check(self.L.hp_lz_combine(self.nloc[i], mm, ctypes.cast(ptrs, ctypes.c_void_p), self._vp(st),
+                                                self._vp(out[i]), self.nat.stream_ptr()))
+
+    def lz_diag(self, st):
+        import torch
+
+        d = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.nat.check(self.L.hp_lz_diag(self._vp(st), self._vp(d), None, None, self.nat.stream_ptr()))
+        return d
 
 
 def sharded_propagate(shards, fh, ys, t0: float, h: float, nsteps: int, m: int, *, reduce=dist_sum,
@@ -347,16 +447,17 @@ def sharded_propagate(shards, fh, ys, t0: float, h: float, nsteps: int, m: int, 
     halos are refreshed by each matvec's exchange), ``fh`` the FastHamiltonian of the full cube
     (its surrogate is re-interpolated at every step's midpoint, as the reference does).  Every
     vector operation runs on the owned planes of each shard; Lanczos dot products and norms are
-    per-shard partials combined by ``reduce`` (all-gather + rank-ordered sum), so every rank
-    holds identical alpha, beta.
+    per-shard partials combined by ``reduce`` (all-gather + rank-ordered sum, on the device), so
+    every rank holds identical alpha, beta.
 
-    The basis is kept unnormalised (u_k = v_k / s_k with known s_k) and box-sized (the matvec
-    reads it in place), so a Lanczos iteration is the sharded matvec on u_k, one dot and one
-    fused update + norm pass (u_{k+1} = s_k A u_k - alpha_k s_k u_k - beta_{k-1} s_{k-1}
-    u_{k-1}); alpha comes out of the matvec itself when the fused kernel applies (its in-kernel
-    rows of u^H A u, hp_apply_polynomial_planes_dot), otherwise from one dot pass.  The step
-    ends with one combine pass written over the state.  ``ops`` supplies
-    the per-shard kernels (default DeviceStepOps).  Returns ``ys`` advanced in place.
+    The basis is kept unnormalised (u_k = v_k / s_k) and box-sized (the matvec reads it in place),
+    so a Lanczos iteration is the sharded matvec on u_k -- alpha from its in-kernel rows of
+    u^H A u (hp_apply_hamiltonian_planes_dot, the harmonic part folded in), else one dot pass --
+    and one fused update + norm pass.  Every scalar (alpha, beta, scales, breakdown, the QL and
+    exp column) lives in a device state (hp_lz_*): an iteration is a pure launch + collective
+    sequence with no host round trip.  The step ends with one combine pass written over the
+    state.  ``ops`` supplies the per-shard kernels (default DeviceStepOps).  Returns ``ys``
+    advanced in place; raises RuntimeError on a QL failure (checked once per call).
     """
     ops = ops or DeviceStepOps(shards, ys, fh, exchange)
     ns = len(shards)
@@ -365,37 +466,35 @@ def sharded_propagate(shards, fh, ys, t0: float, h: float, nsteps: int, m: int, 
     def total(parts):
         return reduce([p.clone() for p in parts])
 
+    states = []
     for step in range(nsteps):
         t = t0 + step * h
         ap = ops.approx(t + 0.5 * h)
         y = [ys[i][own[i]] for i in range(ns)]
-        nrm0 = float(total(ops.cdot(y, y))[0]) ** 0.5
-        if nrm0 == 0.0:
+        st = ops.lz_new(m)
+        n2 = total(ops.cdot(y, y))
+        if step == 0 and float(n2[0]) == 0.0:  # the one host read of the call
             raise ValueError("starting vector must be nonzero")
+        ops.lz_set(st, 0, "begin", n2, breakdown_tol)
         UB = [list(ys)]  # u_0 = y itself, s_0 = 1 / ||y||
         U = [y]
-        s = [1.0 / nrm0]
-        alpha, beta = [], []
         for k in range(m):
             w, dots = ops.matvec(ap, UB[k])
             if dots is None:  # the matvec did not form u_k^H A u_k itself
                 dots = ops.cdot(U[k], w)
-            alpha.append(s[k] * s[k] * float(total(dots)[0]))  # s_k^2 u_k^H A u_k
+            ops.lz_set(st, k, "alpha", total(dots), breakdown_tol)
             if k == m - 1:
                 break
             nb = [ops.new_box(x) for x in ys]
             nxt = [nb[i][own[i]] for i in range(ns)]
-            cp = -beta[k - 1] * s[k - 1] if k > 0 else 0.0
-            bk = float(total(ops.update(s[k], w, -alpha[k] * s[k], U[k], cp, U[k - 1] if k > 0 else None,
-                                        nxt))[0]) ** 0.5
-            if bk <= breakdown_tol:
-                break
-            beta.append(bk)
+            parts = ops.lz_update(st, k, w, U[k], U[k - 1] if k > 0 else None, nxt)
+            ops.lz_set(st, k, "beta", total(parts), breakdown_tol)
             UB.append(nb)
             U.append(nxt)
-            s.append(1.0 / bk)
-        mm = len(alpha)
-        col = ops.expm_col(alpha, beta[:mm - 1], h)
-        # y = ||y|| sum_k col_k v_k = ||y|| sum_k col_k s_k u_k
-        ops.combine(U[:mm], np.array([complex(col[k]) * s[k] * nrm0 for k in range(mm)]), y)
+        ops.lz_finish(st, h)
+        ops.lz_combine(st, U, y)  # y = ||y|| sum_k col_k s_k u_k over the effective basis
+        states.append(st)
+    diags = [ops.lz_diag(st) for st in states]
+    if any(float(d[3]) != 0.0 for d in diags):
+        raise RuntimeError("tridiagonal QL failed to converge")
     return ys

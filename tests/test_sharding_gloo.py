@@ -15,7 +15,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1403_3511_b200.sharding import SlabGeometry, fixed_order_sum, halo_exchange, partition
+from paper_1403_3511_b200.sharding import (HostLanczosScalars, SlabGeometry, fixed_order_sum, halo_exchange,
+                                          partition)
 
 
 def _free_port():
@@ -100,9 +101,10 @@ def test_partition_and_geometry():
     assert ex[1][1] == slice(16 * g.plane, 20 * g.plane) and ex[1][2] == slice(20 * g.plane, 24 * g.plane)
 
 
-class _CpuStepOps:
+class _CpuStepOps(HostLanczosScalars):
     """sharding.sharded_propagate's per-shard kernels on CPU: the oracle's slab Hamiltonian after a
-    gloo halo exchange, numpy dot / update / combine (one shard per process)."""
+    gloo halo exchange, numpy dot / update / combine (one shard per process); the Lanczos scalars
+    follow the device state machine's host restatement."""
 
     def __init__(self, geo, w):
         from oracle import hprop_oracle as O
