@@ -504,6 +504,7 @@ extern "C" {
 
 hp_status hp_apply_coordinate(hp_set_t s, int axis, int dtype, const void* in, void* out, int64_t batch,
                               void* stream) {
+  HP_NVTX("hp_apply_coordinate");
   hp_status rc = check_set(s);
   if (rc) return rc;
   if (axis < 1 || axis > s->dim)
@@ -531,6 +532,7 @@ size_t hp_cheb_workspace_bytes(hp_set_t s, int dtype, int64_t batch) {
 
 hp_status hp_cheb_apply(hp_set_t s, int axis, int degree, double halfwidth, int dtype, const void* in,
                         void* out, int64_t batch, void* ws, size_t ws_bytes, void* stream) {
+  HP_NVTX("hp_cheb_apply");
   hp_status rc = check_set(s);
   if (rc) return rc;
   if (axis < 1 || axis > s->dim)
@@ -600,6 +602,7 @@ hp_status hp_apply_polynomial(hp_set_t s, const int32_t* degrees, const double* 
                               double halfwidth, int dtype, const void* in, void* out, int64_t batch,
                               int flags, const int32_t* axis_order, void* ws, size_t ws_bytes,
                               void* stream) {
+  HP_NVTX("hp_apply_polynomial");
   hp_status rc = check_set(s);
   if (rc) return rc;
   if ((rc = check_terms(s, degrees, nterms, halfwidth))) return rc;
@@ -658,6 +661,7 @@ hp_status hp_apply_polynomial_streamed(hp_set_t s, const int32_t* degrees, const
                                        double halfwidth, int dtype, const void* in_host, void* out_host,
                                        void* in_dev, void* out_dev, int64_t batch, int flags, void* ws,
                                        size_t ws_bytes, void* stream) {
+  HP_NVTX("hp_apply_polynomial_streamed");
   hp_status rc = check_set(s);
   if (rc) return rc;
   if ((rc = check_terms(s, degrees, nterms, halfwidth))) return rc;
@@ -729,6 +733,7 @@ hp_status hp_apply_hamiltonian_planes_dot(hp_set_t s, const int32_t* degrees, co
                                           double halfwidth, double q, int dtype, const void* in, void* out,
                                           int plane_lo, int plane_hi, int flags, double* dot_dev, void* ws,
                                           size_t ws_bytes, void* stream) {
+  HP_NVTX("hp_apply_hamiltonian_planes_dot");
   hp_status rc = check_set(s);
   if (rc) return rc;
   if ((rc = check_terms(s, degrees, nterms, halfwidth))) return rc;
@@ -755,6 +760,7 @@ hp_status hp_apply_polynomial_planes(hp_set_t s, const int32_t* degrees, const d
 }
 
 hp_status hp_square_sum(hp_set_t s, int dtype, const void* in, void* out, int64_t batch, void* stream) {
+  HP_NVTX("hp_square_sum");
   hp_status rc = check_set(s);
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);

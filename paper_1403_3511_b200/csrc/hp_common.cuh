@@ -8,7 +8,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -39,6 +41,32 @@ hp_status cuda_fail(cudaError_t e, const char* what);
     cudaError_t e_ = cudaGetLastError();                \
     if (e_ != cudaSuccess) return hp::cuda_fail(e_, what); \
   } while (0)
+
+// Device-side bounds checks (compute-sanitizer is unavailable on this pool): compiled into the
+// `make checks` variant (libhprop_b200_checks.so, -DHP_DEVICE_CHECKS) only; a failed check traps,
+// which surfaces as a sticky CUDA error in the calling test.
+#ifdef HP_DEVICE_CHECKS
+#define HP_DCHECK(cond)                                                                          \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("HP_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,      \
+             (int)blockIdx.x, (int)threadIdx.x);                                                 \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define HP_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
+// NVTX range around a C-ABI entry point (visible in Nsight timelines; a no-op without a tool
+// attached).  NVTX v3 is header-only.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define HP_NVTX(name) hp::NvtxRange hp_nvtx_range_(name)
 
 // Events of one streamed (host-buffer) call, destroyed on every exit path.  If the call fails
 // after queueing copies on the shared copy streams, the destructor drains those streams first,

@@ -232,6 +232,8 @@ __global__ void __launch_bounds__(Q_NT, 1)
         if (p < pe) {
           f1_mbar_wait(&full[cs], (unsigned)(cu & 1));
           const double2* st = stg + (size_t)cs * Q_STAGE;
+          HP_DCHECK(oc - 4 * Q_R1 >= 0 && oc + 6 * Q_R1 + 2 * Q_RW + 4 < Q_A1 && o2a[0] + dlo >= 0 &&
+                    o2a[3] + dhi < Q_STAGE && cs < Q_S);
           // march-axis weights of plane p (uniform over the CTA)
 #define Q3(i) A3[(i) * Q_T3N]
 #define QW(i) W[p * F1_WROW + (i)]
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
             }
             if (p - Q_H >= plo) {
               double2* yb = yq;
+              HP_DCHECK(yb - y >= 0 && yb - y + (in11 ? s1 + s2 : 0) < (int64_t)n0 * plane);
               if (in00) __stcs(yb, R[0][SQ]);
               if (in10) __stcs(yb + s1, R[1][SQ]);
               if (in01) __stcs(yb + s2, R[2][SQ]);

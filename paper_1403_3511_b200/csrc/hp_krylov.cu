@@ -848,6 +848,7 @@ size_t hp_magnus_workspace_bytes(hp_set_t s, int scheme, const int32_t* d1, int 
 hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* d1, const double* c1, int n1, const int32_t* d2,
                          const double* c2, int n2, double halfwidth, double q, double h, int m, int reorth,
                          void* y, double* diag, void* ws, size_t ws_bytes, void* stream) {
+  HP_NVTX("hp_magnus_step");
   if (!s) return fail(HP_ERR_VALUE, "null set handle");
   hp_status rc = check_m(m);
   if (rc) return rc;
@@ -912,6 +913,7 @@ hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* d1, const double
 hp_status hp_lanczos(hp_set_t s, const int32_t* d, const double* c, int nterms, double halfwidth, double q,
                      const void* v0, int steps, int reorth, void* basis, double* alpha, double* beta, double* diag,
                      void* ws, size_t ws_bytes, void* stream) {
+  HP_NVTX("hp_lanczos");
   if (!s) return fail(HP_ERR_VALUE, "null set handle");
   hp_status rc = check_m(steps);
   if (rc) return rc;

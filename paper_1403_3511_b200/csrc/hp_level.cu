@@ -379,7 +379,10 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
         };
         double2 Tm[S], Tc[S], Tn[S];
 #pragma unroll
-        for (int p = 0; p < S; ++p) Tm[p] = seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
+        for (int p = 0; p < S; ++p) {
+          HP_DCHECK(seg[p] < n);
+          Tm[p] = seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
+        }
         emit(0, Tm[K]);
 #pragma unroll
         for (int k = 1; k <= K; ++k) {

@@ -55,6 +55,7 @@ __global__ void k_restrict(int64_t n, int64_t nfull, int64_t batch, PosMap m, co
                            T* __restrict__ sub) {
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = m.pos(o);
+    HP_DCHECK(p >= 0 && p < nfull);
     for (int64_t b = 0; b < batch; ++b) sub[b * n + o] = __ldg(full + b * nfull + p);
   }
 }
@@ -64,6 +65,7 @@ __global__ void k_extend(int64_t n, int64_t nfull, int64_t batch, PosMap m, cons
                          T* __restrict__ full) {
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = m.pos(o);
+    HP_DCHECK(p >= 0 && p < nfull);
     for (int64_t b = 0; b < batch; ++b) full[b * nfull + p] = __ldg(sub + b * n + o);
   }
 }
@@ -130,6 +132,7 @@ extern "C" {
 
 hp_status hp_restrict(hp_set_t sub, hp_set_t full, int dtype, const void* full_dev, void* sub_dev, int64_t batch,
                       void* stream) {
+  HP_NVTX("hp_restrict");
   hp_status rc = check_pair(sub, full);
   if (rc) return rc;
   if (sub->n == 0 || batch <= 0) return HP_OK;
@@ -146,6 +149,7 @@ hp_status hp_restrict(hp_set_t sub, hp_set_t full, int dtype, const void* full_d
 
 hp_status hp_extend(hp_set_t sub, hp_set_t full, int dtype, const void* sub_dev, void* full_dev, int64_t batch,
                     void* stream) {
+  HP_NVTX("hp_extend");
   hp_status rc = check_pair(sub, full);
   if (rc) return rc;
   if (batch <= 0) return HP_OK;
@@ -165,6 +169,7 @@ hp_status hp_extend(hp_set_t sub, hp_set_t full, int dtype, const void* sub_dev,
 
 hp_status hp_reduction_components(hp_set_t sub, hp_set_t full, int dtype, const void* on_set_dev,
                                   const void* on_full_dev, double* comp_dev, void* stream) {
+  HP_NVTX("hp_reduction_components");
   hp_status rc = check_pair(sub, full);
   if (rc) return rc;
   if (sub->n == 0) return HP_OK;
@@ -183,6 +188,7 @@ hp_status hp_reduction_components(hp_set_t sub, hp_set_t full, int dtype, const 
 
 hp_status hp_reduction_local_mask(hp_set_t s, const int32_t* degrees_host, int nterms, uint8_t* mask_dev,
                                   void* stream) {
+  HP_NVTX("hp_reduction_local_mask");
   if (!s) return fail(HP_ERR_VALUE, "null set handle");
   if (nterms < 0) return fail(HP_ERR_VALUE, "nterms must be nonnegative");
   for (int64_t i = 0; i < (int64_t)nterms * s->dim; ++i)

@@ -305,6 +305,7 @@ hp_status hp_set_create_slab(int dim, int bound, int lo, int hi, void* stream, h
 }
 
 hp_status hp_set_create_hyperbolic(int dim, int bound, void* stream, hp_set_t* out, int64_t* n_out) {
+  HP_NVTX("hp_set_create_hyperbolic");
   if (dim <= 0) return fail(HP_ERR_VALUE, "dimension must be positive, got " + std::to_string(dim));
   if (bound < 0) return fail(HP_ERR_VALUE, "bound must be nonnegative, got " + std::to_string(bound));
   if (dim > HP_MAXDIM) return fail(HP_ERR_VALUE, "dimension exceeds HP_MAXDIM");
@@ -352,6 +353,7 @@ hp_status hp_set_create_hyperbolic(int dim, int bound, void* stream, hp_set_t* o
 
 hp_status hp_set_create_custom(int dim, int bound, const int64_t* indices_host, int64_t n,
                                void* stream, hp_set_t* out) {
+  HP_NVTX("hp_set_create_custom");
   if (dim <= 0) return fail(HP_ERR_VALUE, "dimension must be positive, got " + std::to_string(dim));
   if (bound < 0) return fail(HP_ERR_VALUE, "bound must be nonnegative, got " + std::to_string(bound));
   if (dim > HP_MAXDIM) return fail(HP_ERR_VALUE, "dimension exceeds HP_MAXDIM");
