@@ -30,7 +30,9 @@ w3 = W.CONFIGS["cfg3"].scaled(63)
 s3 = hp.build_hyperbolic(6, 63)
 ap3 = w3.approx(0.0, validate=False)
 v3 = torch.randn(s3.size, dtype=torch.complex128, device="cuda")
-hp.reduction_error(s3, ap3, hp.CoeffVector(s3, v3))
+sr = hp.build_hyperbolic(4, 15)  # reduction error extends to the full cube: keep it small
+vr = torch.randn(sr.size, dtype=torch.complex128, device="cuda")
+hp.reduction_error(sr, hp.interpolate(hp.potential_by_name("henon-heiles", 4), 3), hp.CoeffVector(sr, vr))
 fh = hp.FastHamiltonian(s3, hp.custom_potential(w3.evaluator, 6, 16.0), 2)
 fh.propagate(hp.MagnusScheme.from_name("midpoint"), v3, 0.0, 0.001, 2, 7)
 fh4 = hp.FastHamiltonian(s4, hp.custom_potential(w4.evaluator, 4, 16.0), 4)
