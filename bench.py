@@ -468,7 +468,8 @@ def gpu_arm(args, rank, world, local_rank):
                                            f"skipped, {sharding.schedule()} schedule; value = that rank's planes/s)")
                            if emu else f"slab-j1 x{world}" if sharding is not None else
                            ("single" if world == 1 else f"batch/{world}" if part else f"replicas x{world}")},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roofline, "fp64": fp64_utilisation(w.name, ms_step) if not emu and world == 1 else None,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "propagation": prop}
         print(json.dumps(line), flush=True)
 
@@ -594,13 +595,29 @@ def propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind, sharded):
     return out if rank == 0 else None
 
 
+def _profile_record():
+    p = ROOT / "profiles" / "traffic.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
 def profiled_traffic(workload: str):
     """dram read+write bytes per matvec from the committed ncu capture, if any."""
-    p = ROOT / "profiles" / "traffic.json"
-    if p.exists():
-        d = json.loads(p.read_text())
-        return d.get(workload)
-    return None
+    return _profile_record().get(workload)
+
+
+def fp64_utilisation(workload: str, ms_step: float):
+    """FP64 rate of the step against the measured DFMA peak: the step's FP64 flops are the ncu
+    instruction counts of its kernels (committed with the capture; the kernels' flop count per
+    matvec is fixed by the term list, not by the run), divided by this run's step time."""
+    rec = _profile_record()
+    flops = (rec.get("fp64_flops") or {}).get(workload)
+    peak = rec.get("fp64_peak_tflops")
+    if not flops or not peak:
+        return None
+    ach = flops / (ms_step * 1e-3) / 1e12
+    return {"flops_per_step": flops, "achieved_tflops": round(ach, 3), "peak_tflops": peak,
+            "frac": round(ach / peak, 4), "peak_kind": "measured (tools/microbench.cu DFMA chain)",
+            "source": "ncu 2 x dfma + dadd + dmul thread instructions of the step's kernels (profiles/traffic.json)"}
 
 
 def step_mode(args, w, rank, world, local_rank, hbm, peak_kind):
