@@ -210,6 +210,10 @@ hp_status hp_extend(hp_set_t subset, hp_set_t full, int dtype, const void* sub_d
 hp_status hp_reduction_components(hp_set_t subset, hp_set_t full, int dtype, const void* on_set_dev,
                                   const void* on_full_dev, double* comp_dev, void* stream);
 
+/* make_decay_vector's unnormalised entries -- error_lab.py:43-56: out[o] = prod_l max(j_l, 1)^(-beta)
+ * (float64, the set's order); HP_ERR_VALUE for beta < 1. */
+hp_status hp_decay_vector(hp_set_t s, int beta, double* out_dev, void* stream);
+
 /* reduction_local_mask -- error_lab.py:133-148: mask[o] = 1 iff j(o) + r is in the set for every
  * degree tuple r of the term list (up-walks through the neighbour tables; bound test on cubes).
  * Synchronises the stream. */

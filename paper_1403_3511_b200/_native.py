@@ -74,6 +74,7 @@ SIGNATURES = {
     "hp_extend": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_i64, c_vp]),
     "hp_reduction_components": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),
     "hp_reduction_local_mask": (c_int, [c_vp, c_i32p, c_int, c_vp, c_vp]),
+    "hp_decay_vector": (c_int, [c_vp, c_int, c_vp, c_vp]),
     "hp_magnus_workspace_bytes": (c_sz, [c_vp, c_int, c_i32p, c_int, c_i32p, c_int, c_int]),
     "hp_magnus_step": (c_int, [c_vp, c_int, c_i32p, c_dblp, c_int, c_i32p, c_dblp, c_int, c_dbl, c_dbl,
                                c_dbl, c_int, c_int, c_vp, c_vp, c_vp, c_sz, c_vp]),

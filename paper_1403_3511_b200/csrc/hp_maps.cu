@@ -113,6 +113,16 @@ __global__ void k_local_mask(int64_t n, int dim, int boxed, PosMap m, int bound,
   }
 }
 
+// make_decay_vector's entries (error_lab.py:43-56): prod_l max(j_l, 1)^(-beta), normalised by the
+// caller's device norm pass
+__global__ void k_decay(int64_t n, int dim, PosMap m, double mbeta, double* __restrict__ out) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+    double p = 1.0;
+    for (int a = 0; a < dim; ++a) p *= pow((double)max(m.j(a, o), 1), mbeta);
+    out[o] = p;
+  }
+}
+
 static hp_status check_pair(const hp_set_s* sub, const hp_set_s* full) {
   if (!sub || !full) return fail(HP_ERR_VALUE, "null set handle");
   if (full->kind != HP_KIND_FULL || !full->boxed || full->lo != 0 || full->hi != full->bound + 1)
@@ -183,6 +193,16 @@ hp_status hp_reduction_components(hp_set_t sub, hp_set_t full, int dtype, const 
     k_reduction_components<double><<<grid, 256, 0, st>>>(sub->n, m, (const double*)on_set_dev,
                                                           (const double*)on_full_dev, comp_dev);
   HP_LAUNCH_CHECK("k_reduction_components");
+  return HP_OK;
+}
+
+hp_status hp_decay_vector(hp_set_t s, int beta, double* out_dev, void* stream) {
+  HP_NVTX("hp_decay_vector");
+  if (!s) return fail(HP_ERR_VALUE, "null set handle");
+  if (beta < 1) return fail(HP_ERR_VALUE, "beta must be a positive integer, got " + std::to_string(beta));
+  if (s->n == 0) return HP_OK;
+  k_decay<<<grid_for(s->n, 256), 256, 0, as_stream(stream)>>>(s->n, s->dim, pos_map(s), -(double)beta, out_dev);
+  HP_LAUNCH_CHECK("k_decay");
   return HP_OK;
 }
 

@@ -113,15 +113,21 @@ def reduction_local_mask(iset: IndexSet, approx: ChebApprox) -> np.ndarray:
     return iset._from_canon(mask).cpu().numpy().astype(bool)
 
 
-def make_decay_vector(iset: IndexSet, beta: int, *, normalized: bool = True) -> CoeffVector:
-    """v_k = prod_l max(k_l, 1)^(-beta) (error_lab.py:43-56)."""
+def make_decay_vector(iset: IndexSet, beta: int, *, normalized: bool = True, device: bool = False) -> CoeffVector:
+    """v_k = prod_l max(k_l, 1)^(-beta), optionally normalised (error_lab.py:43-56), computed on the
+    device from the set's tables (hp_decay_vector) and normalised by the device 2-norm.  Returns
+    host data like the reference; ``device=True`` keeps a CUDA tensor."""
+    import torch
+
     if beta < 1:
         raise ValueError(f"beta must be a positive integer, got {beta}")
-    base = np.maximum(iset.indices, 1).astype(np.float64)
-    data = np.prod(base ** (-float(beta)), axis=1)
+    d = torch.empty(iset.size, dtype=torch.float64, device="cuda")
+    nat.check(nat.lib().hp_decay_vector(ctypes.c_void_p(iset.handle), int(beta), ctypes.c_void_p(d.data_ptr()),
+                                        nat.stream_ptr()))
+    d = iset._from_canon(d)
     if normalized:
-        data = data / np.linalg.norm(data)
-    return CoeffVector(iset, data)
+        d = d / torch.linalg.vector_norm(d)
+    return CoeffVector(iset, d if device else d.cpu().numpy())
 
 
 class _HamMatVec:

@@ -6,6 +6,7 @@ Runs the REFERENCE (imported read-only) on small cases:
 
 * ``reduction_error`` components and ``reduction_local_mask`` (error_lab.py:114-148) on
   hyperbolic sets with the reference's decay vector (error_lab.py:43-56);
+* ``make_decay_vector`` (error_lab.py:43-56) on three sets;
 * the CSV text of ``hprop rederr`` (cli.py:299-314) for two argument lists, to compare the
   device CLI's columns and values against.
 """
@@ -38,6 +39,10 @@ def main():
         g[key + "_comp"] = rep.components
         g[key + "_mask"] = error_lab.reduction_local_mask(s, ap)
         g[key + "_max"] = np.float64(rep.max_norm)
+    for kind, dim, bound, beta, norm in [("hyperbolic", 3, 10, 2, True), ("full", 2, 7, 3, True),
+                                         ("hyperbolic", 4, 8, 1, False)]:
+        s = (hprop.build_hyperbolic if kind == "hyperbolic" else hprop.build_full)(dim, bound)
+        g[f"decay_{kind}_{dim}_{bound}_{beta}_{int(norm)}"] = error_lab.make_decay_vector(s, beta, normalized=norm).data
     for i, argv in enumerate(CLI_ARGS):
         buf = io.StringIO()
         with redirect_stdout(buf):

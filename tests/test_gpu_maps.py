@@ -193,3 +193,18 @@ def test_unsorted_custom_set_keeps_the_callers_order(hp):
     # a pinned host tensor comes back as a host tensor
     yt = fu.propagate(sch, torch.from_numpy(v).pin_memory(), 0.0, 0.01, 2, 6)
     assert not yt.is_cuda and rel_l2(yt.numpy(), fc.propagate(sch, vc, 0.0, 0.01, 2, 6)[perm]) <= 1e-13
+
+
+def test_decay_vector_matches_reference(hp, gold):
+    import torch
+
+    for key in [k for k in gold if k.startswith("decay_")]:
+        _, kind, dim, bound, beta, norm = key.split("_")
+        s = (hp.build_hyperbolic if kind == "hyperbolic" else hp.build_full)(int(dim), int(bound))
+        v = hp.make_decay_vector(s, int(beta), normalized=bool(int(norm)))
+        assert isinstance(v.data, np.ndarray)
+        assert np.max(np.abs(v.data - gold[key])) <= 1e-15 * np.max(np.abs(gold[key]))
+        d = hp.make_decay_vector(s, int(beta), normalized=bool(int(norm)), device=True)
+        assert d.data.is_cuda and torch.equal(d.data.cpu(), torch.from_numpy(v.data))
+    with pytest.raises(ValueError, match="positive integer"):
+        hp.make_decay_vector(hp.build_full(2, 3), 0)
