@@ -1,6 +1,6 @@
 """pytest plugin: run the REFERENCE's own test modules with the device applier installed.
 
-    python -m pytest -p tests.ref_suite_plugin baseline/_ref/tests/test_fast_apply.py ...
+    PYTHONPATH=tests python -m pytest -p ref_suite_plugin baseline/_ref/tests/test_fast_apply.py ...
 
 Every index set the reference tests build gets the B200 applier on first use: the plugin
 replaces `hprop.fast_apply.get_applier` (fast_apply.py:248-254, the seam every caller resolves

@@ -13,6 +13,7 @@ The modules come from baseline/_ref/tests (tools/install_reference.sh copies the
 installed package; git-ignored, shipped to the GPU box with the snapshot).
 """
 
+import os
 import re
 import subprocess
 import sys
@@ -30,9 +31,10 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not (SUITE / "test_fast_apply.
 
 
 def test_reference_suite_passes_on_the_device_applier():
-    cmd = [sys.executable, "-m", "pytest", "-p", "tests.ref_suite_plugin", "-q", "-p", "no:cacheprovider",
+    cmd = [sys.executable, "-m", "pytest", "-p", "ref_suite_plugin", "-q", "-p", "no:cacheprovider",
            "--rootdir", str(SUITE)] + [str(SUITE / m) for m in MODULES]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1800)
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([str(ROOT / "tests"), os.environ.get("PYTHONPATH", "")]))
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1800, env=env)
     tail = r.stdout[-3000:] + r.stderr[-2000:]
     assert r.returncode == 0, tail
     m = re.search(r"device appliers installed: (\d+)", r.stdout)
