@@ -313,11 +313,11 @@ def gpu_arm(args, rank, world, local_rank):
     part = world > 1 and sharding is None and w.batch > 1
     if sharding is not None:
         c_host = sharding.local_coefficients(W, w)
+    elif part:  # this rank's vectors only (the other ranks' draws are discarded)
+        b0, b1 = rank * w.batch // world, (rank + 1) * w.batch // world
+        c_host = W.coefficients_rows(w, s.indices, b0, b1)
     else:
         c_host = W.coefficients(w, None if w.kind == "full" else s.indices)
-        if part:
-            b0, b1 = rank * w.batch // world, (rank + 1) * w.batch // world
-            c_host = np.ascontiguousarray(c_host[b0:b1])
     x = torch.from_numpy(c_host).to(dev)
     y = torch.empty_like(x)
     batch = c_host.shape[0] if part else w.batch

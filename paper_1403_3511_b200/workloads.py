@@ -210,32 +210,41 @@ def _normalise(row: np.ndarray, chunk: int) -> None:
     row /= math.sqrt(sq)
 
 
-def coefficients_row(w: Workload, indices: np.ndarray | None, row: int, chunk: int = 1 << 24) -> np.ndarray:
-    """Row ``row`` of ``coefficients(w, indices)``, bit-identical, without the whole batch.
-
-    The seeded stream is drawn in the same chunks as ``coefficients`` and the
-    draws of the other rows are discarded (cfg5: 0.4 GB instead of 13 GB).
-    """
+def coefficients_rows(w: Workload, indices: np.ndarray | None, lo: int, hi: int,
+                      chunk: int = 1 << 24) -> np.ndarray:
+    """Rows [lo, hi) of ``coefficients(w, indices)`` (shape (hi - lo, n)), bit-identical, without
+    the rest of the batch: the seeded stream is drawn in the same chunks as ``coefficients`` and
+    the other rows' draws are discarded (a cfg5 rank of a batch-partitioned run holds 4 of the
+    32 rows: 1.6 GB instead of 13 GB)."""
     n = w.size()
-    if not 0 <= row < w.batch:
-        raise ValueError("row out of range")
+    if not 0 <= lo < hi <= w.batch:
+        raise ValueError("row range out of bounds")
     rng = np.random.default_rng([w.seed, 0])
     total = w.batch * n
-    out = np.empty(n, dtype=np.complex128)
-    lo, hi = row * n, (row + 1) * n
+    out = np.empty((hi - lo, n), dtype=np.complex128)
+    flat = out.reshape(-1)
+    a0, a1 = lo * n, hi * n
     for part in ("re", "im"):
         for s in range(0, total, chunk):
             e = min(total, s + chunk)
             vals = rng.standard_normal(e - s)
-            a, b = max(s, lo), min(e, hi)
+            a, b = max(s, a0), min(e, a1)
             if a < b:
                 if part == "re":
-                    out.real[a - lo:b - lo] = vals[a - s:b - s]
+                    flat.real[a - a0:b - a0] = vals[a - s:b - s]
                 else:
-                    out.imag[a - lo:b - lo] = vals[a - s:b - s]
+                    flat.imag[a - a0:b - a0] = vals[a - s:b - s]
     for s in range(0, n, chunk):
         e = min(n, s + chunk)
         idx = _full_rows(w.dim, w.bound, s, e) if w.kind == "full" else indices[s:e]
-        out[s:e] *= decay_values(w.decay, idx)
-    _normalise(out, chunk)
+        out[:, s:e] *= decay_values(w.decay, idx)[None, :]
+    for r in range(out.shape[0]):
+        _normalise(out[r], chunk)
     return out
+
+
+def coefficients_row(w: Workload, indices: np.ndarray | None, row: int, chunk: int = 1 << 24) -> np.ndarray:
+    """Row ``row`` of ``coefficients(w, indices)``, bit-identical (see coefficients_rows)."""
+    if not 0 <= row < w.batch:
+        raise ValueError("row out of range")
+    return coefficients_rows(w, indices, row, row + 1, chunk)[0]
