@@ -133,7 +133,7 @@ struct Builder {
 
 }  // namespace
 
-static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut) {
+static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut, bool merge_enabled) {
   LvProgram P;
   const int BUF_V_ = -2, BUF_Y_ = -1;
   int next_slot = 0;
@@ -172,32 +172,83 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut)
     std::vector<int> inputs;
     for (auto& nd : nodes) if (nd.buf >= 0) inputs.push_back(nd.buf);
     if (!y_written) for (int it : consts) B.add(BUF_Y_, BUF_V_, 0, terms[it].alpha);
-    std::vector<Node> next;
-    std::vector<int> released;
+    // candidate next nodes: T_k(X_a) u_parent (k > 0: a new vector) or u_parent itself (k = 0)
+    struct Cand {
+      int parent, k;
+      std::vector<int> rows;
+    };
+    std::vector<Cand> cands;
     for (auto& nd : nodes) {
       std::map<int, std::vector<int>> groups;
-      std::vector<int> pass;
       for (int it : nd.rows) {
         int k = terms[it].r[a];
         if (k > LV_MAXK) return P;
-        if (k == 0) pass.push_back(it);  // cannot be a leaf: some r[0..a-1] != 0
-        else groups[k].push_back(it);
+        groups[k].push_back(it);
       }
       for (auto& g : groups) {
-        int k = g.first;
+        const int k = g.first;
         std::vector<int> nonleaf;
         for (int it : g.second) {
-          if (zero_upto(terms[it], a - 1)) B.add(BUF_Y_, nd.buf, k, terms[it].alpha);
-          else nonleaf.push_back(it);
+          if (k > 0 && zero_upto(terms[it], a - 1)) B.add(BUF_Y_, nd.buf, k, terms[it].alpha);
+          else nonleaf.push_back(it);  // k == 0 rows cannot be leaves: some r[0..a-1] != 0
         }
-        if (!nonleaf.empty()) {
-          int s = alloc(inputs);
-          B.add(s, nd.buf, k, 1.0);
-          next.push_back({s, nonleaf});
+        if (!nonleaf.empty()) cands.push_back({nd.buf, k, nonleaf});
+      }
+    }
+    // Merge candidates whose remaining term patterns (r_0 .. r_{a-1}) carry proportional
+    // coefficients: every later level would apply them identically, so one accumulated vector
+    // m = u_1 + lambda u_2 + ... replaces them (the representative's terms stand for all).  For
+    // cfg3's equal pair coefficients this turns the per-axis suffix vectors into one running sum;
+    // single-term suffixes with the same remaining pattern merge on any set.
+    auto signature = [&](const std::vector<int>& rows) {
+      std::map<std::vector<int>, double> sig;
+      for (int it : rows) sig[std::vector<int>(terms[it].r, terms[it].r + a)] = terms[it].alpha;
+      return sig;
+    };
+    struct Group {
+      std::map<std::vector<int>, double> sig;
+      std::vector<std::pair<int, double>> members;  // (candidate, lambda)
+    };
+    std::vector<Group> groups;
+    for (int ci = 0; ci < (int)cands.size(); ++ci) {
+      auto sig = signature(cands[ci].rows);
+      bool placed = !merge_enabled;
+      for (auto& gr : groups) {
+        if (placed) break;
+        if (gr.sig.size() != sig.size()) continue;
+        const double lam = sig.begin()->second / gr.sig.begin()->second;
+        bool prop = true;
+        for (auto ia = gr.sig.begin(), ib = sig.begin(); prop && ia != gr.sig.end(); ++ia, ++ib)
+          prop = ia->first == ib->first && std::fabs(ib->second - lam * ia->second) <= 1e-15 * std::fabs(ib->second);
+        if (prop) {
+          gr.members.push_back({ci, lam});
+          placed = true;
         }
       }
-      if (!pass.empty()) next.push_back({nd.buf, pass});
-      else if (nd.buf >= 0) released.push_back(nd.buf);
+      if (!placed || !merge_enabled) groups.push_back({sig, {{ci, 1.0}}});
+    }
+    std::vector<Node> next;
+    for (auto& gr : groups) {
+      const Cand& rep = cands[gr.members[0].first];
+      if (gr.members.size() == 1) {
+        if (rep.k == 0) {
+          next.push_back({rep.parent, rep.rows});  // passes through: no new vector
+        } else {
+          int sl = alloc(inputs);
+          B.add(sl, rep.parent, rep.k, 1.0);
+          next.push_back({sl, rep.rows});
+        }
+        continue;
+      }
+      int sl = alloc(inputs);
+      for (auto& mem : gr.members) B.add(sl, cands[mem.first].parent, cands[mem.first].k, mem.second);
+      next.push_back({sl, rep.rows});
+    }
+    std::vector<int> released;
+    for (int buf : inputs) {
+      bool live = false;
+      for (auto& nd : next) live |= nd.buf == buf;
+      if (!live) released.push_back(buf);
     }
     if (!B.finish()) return P;
     // a level whose targets are all directly written child vectors has ntg == 0 but still runs
@@ -206,7 +257,7 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut)
       cost += B.L.nin + B.L.ntg + (B.tg.count(BUF_Y_) && P.levels.size() ? 1 : 0);
       P.levels.push_back(B.L);
     }
-    for (int s : released) free_slots.push_back(s);
+    for (int sl : released) free_slots.push_back(sl);
     nodes = next;
   }
   // ---- cut level: z_pi = sum alpha T_{r_cut}(X_cut) u_sigma, pi = (r_0..r_{cut-1})
@@ -288,16 +339,28 @@ static void dump_plan(const LvProgram& P) {  // HP_LEVEL_DEBUG=1: planner output
   }
 }
 
+static int merge_mode() {  // HP_LEVEL_MERGE=0 disables merging of proportional suffix nodes
+  static int v = [] {
+    const char* e = getenv("HP_LEVEL_MERGE");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 static LvProgram plan_levels(int dim, const std::vector<Term>& terms) {
   LvProgram best;
   if (const char* e = getenv("HP_LEVEL_CUT")) {  // experiments: force the suffix/prefix cut
     int c = atoi(e);
-    if (c >= 0 && c < dim) return plan_with_cut(dim, terms, c);
+    if (c >= 0 && c < dim) return plan_with_cut(dim, terms, c, merge_mode() != 0);
   }
-  for (int cut = 0; cut < dim; ++cut) {
-    LvProgram P = plan_with_cut(dim, terms, cut);
-    if (P.ok && (!best.ok || P.cost < best.cost)) best = std::move(P);
-  }
+  // every cut, with and without merging proportional suffix nodes (merged plans can exceed the
+  // per-level target limit); the cheapest plan wins
+  for (int cut = 0; cut < dim; ++cut)
+    for (int mg = 0; mg < 2; ++mg) {
+      if (mg == 1 && merge_mode() == 0) continue;
+      LvProgram P = plan_with_cut(dim, terms, cut, mg == 1);
+      if (P.ok && (!best.ok || P.cost < best.cost)) best = std::move(P);
+    }
   return best;
 }
 
