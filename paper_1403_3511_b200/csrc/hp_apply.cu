@@ -180,7 +180,9 @@ static int g_blocks(int64_t n) { return grid_for(n, 256, 148 * 16); }
 static size_t chunk_cap() {
   static size_t v = [] {
     const char* e = getenv("HP_CHUNK_GB");
-    return (size_t)(e ? std::max(1, atoi(e)) : 48) << 30;  // cfg5: 24 GiB 830 ms, 48 GiB 795 ms, 64 GiB 801 ms
+    // cfg5, round-1 plans: 24 GiB 830 ms, 48 GiB 795, 64 GiB 801; merged plans (24 slots): 32 GiB 729 ms,
+    // 48 737, 64 744, 96 779 (profiles/r2/sweep_level.txt)
+    return (size_t)(e ? std::max(1, atoi(e)) : 32) << 30;
   }();
   return v;
 }

@@ -596,18 +596,18 @@ __global__ void k_line_heads_list(int64_t n, const int32_t* __restrict__ down, c
     if (__ldg(down + o) < 0) heads[__ldg(pos + o)] = (int32_t)o;
 }
 
-// axes whose level kernels run in line order (HP_LEVEL_PERM: bit a = axis a).  Default: axis 1
-// of sets with N >= 4.  Measured (ms per matvec, ordinal order -> line order of the axes in the
-// mask): cfg3 7.49 -> {1} 7.27, {0,1} 7.39, {0,1,2} 7.53, {0} 7.57; cfg5 (32 vectors) 940 ->
-// {1} 835, {0,1} 831, {0,1,2} 830, {0} 936.  Axis 0 gains nothing (its level has one input and
-// its lines are the longest); axis 1 carries the widest levels of both plans.
+// axes whose level kernels run in line order (HP_LEVEL_PERM: bit a = axis a).  Measured with the
+// merged plans of round 2 (ms per matvec; profiles/r2/sweep_level.txt): cfg3 (N = 6) no axis 6.23,
+// {1} 6.42, {0,1} 6.53, {1,2} 6.65; cfg5 (N = 8, 32 vectors) {0,1,2} 708, {1,2} 715, {0,1} 731,
+// {1} 737.  Round 1 (unmerged plans) preferred {1} on both: the line order pays where a level
+// reads many outer-axis windows, which merging made rarer on N = 6.
 static unsigned perm_axes(int dim) {
   static int env = [] {
     const char* e = getenv("HP_LEVEL_PERM");
     return e ? atoi(e) : -1;
   }();
   if (env >= 0) return (unsigned)env;
-  return dim >= 4 ? 2u : 0u;
+  return dim >= 7 ? 7u : 0u;
 }
 
 // perm: the line-blocked order of the ordinals (a permutation of 0..n-1: every ordinal lies on
