@@ -393,15 +393,24 @@ __global__ void __launch_bounds__(256) k_level(int64_t n, int64_t batch, AX ax, 
                                                const int32_t* __restrict__ perm) {
   constexpr int S = 2 * K + 1;
   double2 dacc = make_double2(0.0, 0.0);
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    // perm (outer axes of tabled sets): line-blocked order (line_order below), so the +-K
-    // windows of neighbouring warps overlap in L1/L2 (ordinal order puts the window positions
-    // one sub-block apart, far beyond L2 reuse)
-    const int64_t o = perm ? (int64_t)__ldg(perm + t) : t;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // perm (outer axes of tabled sets): line-blocked order (line_order below), so the +-K
+  // windows of neighbouring warps overlap in L1/L2 (ordinal order puts the window positions
+  // one sub-block apart, far beyond L2 reuse)
+  int64_t o_next = t < n ? (perm ? (int64_t)__ldg(perm + t) : t) : 0;
+  typename AX::Pre pre_next = ax.pre(o_next);
+  for (; t < n; t += gstride) {
+    const int64_t o = o_next;
+    const typename AX::Pre pre_o = pre_next;
+    if (t + gstride < n) {  // the next ordinal's first walk hop, in flight during this one
+      o_next = perm ? (int64_t)__ldg(perm + t + gstride) : t + gstride;
+      pre_next = ax.pre(o_next);
+    }
     // the axis line through o: seg[K + d] = ordinal of j + d e_a, or -1
     int64_t seg[S];
     int jo;
-    ax.template segment<K>(o, jo, seg);
+    ax.template segment_pre<K>(pre_o, o, jo, seg);
     // ladder coefficients of the window, sq[p] = sqrt(j_p / 2) (cd at p, cu at p - 1); positions
     // with j < 0 are absent (forced to zero below).  Computed, not tabled: a table load would sit
     // on the dependent chain behind the j load (measured slower on cfg3)
@@ -530,7 +539,18 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
   } else {
     LvAllTab axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
-    if (lv.ntg <= 1)
+    if (batch == 1) {
+      const AxTabPf ax(s->tab(lv.axis));
+      if (lv.ntg <= 1)
+        k_level<K, 1, AxTabPf, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
+                                                              slots, y, first, osc, dotp, perm);
+      else if (lv.ntg <= 4)
+        k_level<K, 4, AxTabPf, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
+                                                              slots, y, first, osc, dotp, perm);
+      else
+        k_level<K, LV_MAXTG, AxTabPf, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L,
+                                                                     2.0 / L, v, slots, y, first, osc, dotp, perm);
+    } else if (lv.ntg <= 1)
       k_level<K, 1, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv, 1.0 / L,
                                                           2.0 / L, v, slots, y, first, osc, dotp, perm);
     else if (lv.ntg <= 4)
