@@ -196,6 +196,28 @@ struct AxTab {
   }
 };
 
+// The innermost axis of a tabled (lexicographic, downward-closed) set: its lines are contiguous
+// ordinal runs starting at j = 0, so j - d e_N is o - d whenever j >= d, and o + d lies on the
+// same line iff its own j equals j + d (the next line restarts at 0).  The window is formed from
+// the j table alone -- K + 1 independent, coalesced loads instead of the dependent down/up walk.
+struct AxInner : AxTab {
+  AxInner() = default;
+  explicit AxInner(const AxTab& t, int64_t n_) : AxTab(t), n(n_) {}
+  int64_t n;
+  struct Pre {};
+  __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
+  template <int K>
+  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
+    j = __ldg(jv + o);
+    seg[K] = o;
+#pragma unroll
+    for (int d = 1; d <= K; ++d) {
+      seg[K - d] = j >= d ? o - d : -1;
+      seg[K + d] = (o + d < n && __ldg(jv + o + d) == j + d) ? o + d : -1;
+    }
+  }
+};
+
 // AxTab whose first walk hop is loaded one grid-stride iteration ahead (software pipelining of the
 // dependent table chain: j / down / up of the next ordinal are in flight while the current one's
 // windows are gathered).  Single-vector levels: cfg3 6.24 -> 5.91 ms; a batch of 4 slowed 1%.

@@ -539,7 +539,19 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
   } else {
     LvAllTab axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
-    if (batch == 1) {
+    // innermost axis of a hyperbolic cross (downward closed, lexicographic): windows from the j table
+    if (lv.axis == s->dim - 1 && !perm && s->kind == HP_KIND_HYPERBOLIC) {
+      const AxInner ax(s->tab(lv.axis), n);
+      if (lv.ntg <= 1)
+        k_level<K, 1, AxInner, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
+                                                              slots, y, first, osc, dotp, perm);
+      else if (lv.ntg <= 4)
+        k_level<K, 4, AxInner, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
+                                                              slots, y, first, osc, dotp, perm);
+      else
+        k_level<K, LV_MAXTG, AxInner, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L,
+                                                                     2.0 / L, v, slots, y, first, osc, dotp, perm);
+    } else if (batch == 1) {
       const AxTabPf ax(s->tab(lv.axis));
       if (lv.ntg <= 1)
         k_level<K, 1, AxTabPf, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
