@@ -218,6 +218,29 @@ struct AxInner : AxTab {
   }
 };
 
+// Precomputed windows (hp_level.cu window_table): row r < K holds the ordinal of j - (K - r) e_a,
+// row r >= K that of j + (r - K + 1) e_a (-1 absent), so a level reads 2K independent coalesced
+// ordinals instead of walking the down / up chains (whose second hops are scattered 4-byte reads).
+struct AxWin : AxTab {
+  AxWin() = default;
+  AxWin(const AxTab& t, const int32_t* w, int64_t n_, int kw) : AxTab(t), win(w), n(n_), kwin(kw) {}
+  const int32_t* win;
+  int64_t n;
+  int kwin;  // K of the stored table (>= the level's K)
+  struct Pre {};
+  __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
+  template <int K>
+  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
+    j = __ldg(jv + o);
+    seg[K] = o;
+#pragma unroll
+    for (int d = 1; d <= K; ++d) {
+      seg[K - d] = __ldg(win + (int64_t)(kwin - d) * n + o);
+      seg[K + d] = __ldg(win + (int64_t)(kwin + d - 1) * n + o);
+    }
+  }
+};
+
 // AxTab whose first walk hop is loaded one grid-stride iteration ahead (software pipelining of the
 // dependent table chain: j / down / up of the next ordinal are in flight while the current one's
 // windows are gathered).  Single-vector levels: cfg3 6.24 -> 5.91 ms; a batch of 4 slowed 1%.
@@ -282,6 +305,9 @@ struct hp_set_s {
   // first use by the level kernels of outer axes
   mutable std::mutex perm_mtx;
   mutable int32_t* d_perm[HP_MAXDIM] = {nullptr};
+  // tabled sets: precomputed +-K windows of an axis (hp_level.cu window_table), [2K][n] int32
+  mutable int32_t* d_win[HP_MAXDIM] = {nullptr};
+  mutable int d_win_k[HP_MAXDIM] = {0};
 
   hp::AxBox box(int a) const {
     hp::AxBox v;

@@ -519,6 +519,59 @@ struct LvAllTab {
   __device__ __forceinline__ int j(int a, int64_t o) const { return __ldg(ax[a].jv + o); }
 };
 
+// ---------------------------------------------------------------- precomputed windows
+
+template <int K>
+__global__ void k_build_win(int64_t n, AxTab ax, int32_t* __restrict__ win) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+    int64_t seg[2 * K + 1];
+    int j;
+    ax.template segment<K>(o, j, seg);
+#pragma unroll
+    for (int d = 1; d <= K; ++d) {
+      win[(int64_t)(K - d) * n + o] = (int32_t)seg[K - d];
+      win[(int64_t)(K + d - 1) * n + o] = (int32_t)seg[K + d];
+    }
+  }
+}
+
+static int win_mode() {  // HP_LEVEL_WIN=0: walk the tables in every level (no precomputed windows)
+  static int v = [] {
+    const char* e = getenv("HP_LEVEL_WIN");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+// the +-K windows of axis a, built once per set (and rebuilt for a larger K): 2K int32 per point
+static hp_status window_table(const hp_set_s* s, int a, int K, cudaStream_t st, const int32_t** out, int* kout) {
+  *out = nullptr;
+  if (s->boxed || !win_mode() || K < 1 || s->n < 1 || s->n > INT32_MAX) return HP_OK;
+  std::lock_guard<std::mutex> g(s->perm_mtx);
+  if (!s->d_win[a] || s->d_win_k[a] < K) {
+    if (s->d_win[a]) {
+      HP_CUDA(cudaStreamSynchronize(st));
+      HP_CUDA(cudaFree(s->d_win[a]));
+      s->d_win[a] = nullptr;
+    }
+    int32_t* w = nullptr;
+    HP_CUDA(cudaMalloc(&w, (size_t)2 * K * s->n * sizeof(int32_t)));
+    const int grid = grid_for(s->n, 256);
+    switch (K) {
+      case 1: k_build_win<1><<<grid, 256, 0, st>>>(s->n, s->tab(a), w); break;
+      case 2: k_build_win<2><<<grid, 256, 0, st>>>(s->n, s->tab(a), w); break;
+      case 3: k_build_win<3><<<grid, 256, 0, st>>>(s->n, s->tab(a), w); break;
+      default: k_build_win<4><<<grid, 256, 0, st>>>(s->n, s->tab(a), w); break;
+    }
+    HP_LAUNCH_CHECK("k_build_win");
+    s->d_win[a] = w;
+    s->d_win_k[a] = K;
+  }
+  *out = s->d_win[a];
+  *kout = s->d_win_k[a];
+  return HP_OK;
+}
+
 template <int K>
 static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, const double2* v, double2* slots,
                               double2* y, int64_t batch, int first, int osc, double2* dotp, int grid,
@@ -539,6 +592,7 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
   } else {
     LvAllTab axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
+    int kwin = 0;
     // innermost axis of a hyperbolic cross (downward closed, lexicographic): windows from the j table
     if (lv.axis == s->dim - 1 && !perm && s->kind == HP_KIND_HYPERBOLIC) {
       const AxInner ax(s->tab(lv.axis), n);
@@ -551,6 +605,20 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
       else
         k_level<K, LV_MAXTG, AxInner, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L,
                                                                      2.0 / L, v, slots, y, first, osc, dotp, perm);
+    } else if (const int32_t* win = nullptr;
+               batch > 1 && window_table(s, lv.axis, K, st, &win, &kwin) == HP_OK && win) {
+      // batched levels read precomputed windows (cfg5 713 -> 696 ms); single vectors walk the tables
+      // with the first hop prefetched (cfg3: 5.86 ms vs 6.03 with windows; profiles/r2/sweep_level.txt)
+      const AxWin ax(s->tab(lv.axis), win, n, kwin);
+      if (lv.ntg <= 1)
+        k_level<K, 1, AxWin, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
+                                                            slots, y, first, osc, dotp, perm);
+      else if (lv.ntg <= 4)
+        k_level<K, 4, AxWin, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
+                                                            slots, y, first, osc, dotp, perm);
+      else
+        k_level<K, LV_MAXTG, AxWin, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L,
+                                                                   2.0 / L, v, slots, y, first, osc, dotp, perm);
     } else if (batch == 1) {
       const AxTabPf ax(s->tab(lv.axis));
       if (lv.ntg <= 1)

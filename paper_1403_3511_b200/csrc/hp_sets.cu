@@ -498,6 +498,7 @@ hp_status hp_set_destroy(hp_set_t s) {
     if (s->d_down[a]) cudaFree(s->d_down[a]);
     if (s->d_up[a]) cudaFree(s->d_up[a]);
     if (s->d_perm[a]) cudaFree(s->d_perm[a]);
+    if (s->d_win[a]) cudaFree(s->d_win[a]);
   }
   if (s->d_pref) cudaFree(s->d_pref);
   if (s->d_off) cudaFree(s->d_off);
