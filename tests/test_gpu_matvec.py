@@ -612,11 +612,11 @@ print(worst)
 """
 
 
-@pytest.mark.parametrize("env", [{"HP_FG_QUAD": "0"}, {"HP_FG_RI": "1"}], ids=["k_fg_single", "k_fg_quad_ri"])
+@pytest.mark.parametrize("env", [{"HP_FG_QUAD": "0"}, {"HP_FG_BLOCK": "6,6,4"}], ids=["k_fg_single", "block_664"])
 def test_alternate_single_pass_kernels(env):
-    """The non-default single-pass kernels (selected once per process by environment, so run in a
-    subprocess): k_fg_single (cubes with a side > 128) and the split-component k_fg_quad_ri, on
-    cubes and a j1-slab, against the oracle."""
+    """The non-default single-pass configurations (selected once per process by environment, so
+    run in a subprocess): k_fg_single (cubes with a side > 128) and k_fg_quad with 3-D tile blocks,
+    on cubes and a j1-slab, against the oracle."""
     import os
     import subprocess
     import sys
