@@ -138,16 +138,28 @@ static hp_status reduce(int mode, int64_t n, const double2* a, const double2* b,
 
 // ---------------------------------------------------------------- vector kernels
 
-// gl2 operator average: out = 0.5 (y1 + y2) - i gamma (z2 - z1)  (krylov_propagator.py:226-231)
-__global__ void k_gl2_combine(int64_t n, const double2* __restrict__ y1, const double2* __restrict__ y2,
-                              const double2* __restrict__ z2y1, const double2* __restrict__ z1y2, double gamma,
-                              double2* __restrict__ out) {
+// gl2 operator average: out = 0.5 (y1 + y2) - i gamma (z2 - z1)  (krylov_propagator.py:226-231).
+// With `v` and `dotp`, the block partials of v^H out (the Lanczos alpha of this Krylov matvec) are
+// formed in the same pass -- one extra vector read instead of a separate two-vector dot pass.
+__global__ void __launch_bounds__(256) k_gl2_combine(int64_t n, const double2* __restrict__ y1,
+                                                     const double2* __restrict__ y2,
+                                                     const double2* __restrict__ z2y1,
+                                                     const double2* __restrict__ z1y2, double gamma,
+                                                     double2* __restrict__ out, const double2* __restrict__ v,
+                                                     double2* __restrict__ dotp) {
+  double2 acc = make_double2(0.0, 0.0);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double2 c = ssub(__ldg(z2y1 + i), __ldg(z1y2 + i));
     double2 h = smul(0.5, sadd(__ldg(y1 + i), __ldg(y2 + i)));
     double2 ic = make_double2(__dsub_rn(__dmul_rn(0.0, c.x), __dmul_rn(gamma, c.y)),
                               __dadd_rn(__dmul_rn(0.0, c.y), __dmul_rn(gamma, c.x)));
-    out[i] = ssub(h, ic);
+    const double2 o = ssub(h, ic);
+    out[i] = o;
+    if (dotp) cdot_acc(__ldg(v + i), o, acc);
+  }
+  if (dotp) {
+    acc = block_sum2(acc);
+    if (threadIdx.x == 0) dotp[blockIdx.x] = acc;
   }
 }
 
@@ -893,8 +905,11 @@ hp_status hp_magnus_step(hp_set_t s, int scheme, const int32_t* d1, const double
     if ((r = apply_ham_full(H2, v, y2, tmp, pws, pws_bytes, st))) return r;
     if ((r = apply_ham_full(H2, y1, z2, tmp, pws, pws_bytes, st))) return r;
     if ((r = apply_ham_full(H1, y2, z1, tmp, pws, pws_bytes, st))) return r;
-    k_gl2_combine<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(n, y1, y2, z2, z1, gamma, out);
+    const int gg = grid_for(n, 256, 148 * 16);
+    const bool fuse = dot && dot->partial && gg <= dot->capacity;
+    k_gl2_combine<<<gg, 256, 0, st>>>(n, y1, y2, z2, z1, gamma, out, v, fuse ? dot->partial : nullptr);
     HP_LAUNCH_CHECK("k_gl2_combine");
+    if (fuse) dot->n = gg;
     return HP_OK;
   };
   rc = run_lanczos(s, mv, yv, V, m, reorth != 0, state, partial, dotbuf, w, st);
