@@ -308,6 +308,9 @@ struct hp_set_s {
   // tabled sets: precomputed +-K windows of an axis (hp_level.cu window_table), [2K][n] int32
   mutable int32_t* d_win[HP_MAXDIM] = {nullptr};
   mutable int d_win_k[HP_MAXDIM] = {0};
+  // sqrt(j / 2) for j = -8 .. bound + 8 (entry j at [j + 8]): the ladder coefficients of the level
+  // kernels (hp_level.cu ladder_table); boxes and hyperbolic crosses only (indices <= bound)
+  mutable double* d_sqtab = nullptr;
 
   hp::AxBox box(int a) const {
     hp::AxBox v;

@@ -39,6 +39,8 @@ namespace hp {
 constexpr int LV_MAXIN = 64;
 constexpr int LV_MAXTG = 16;  // targets accumulate in registers
 constexpr int LV_MAXENT = 160;
+constexpr int LV_MAXDIRECT = 48;
+constexpr int LV_WT = 640;  // dense weights: nin * (K + 1) * tgn doubles
 constexpr int LV_MAXK = 4;
 
 struct LvEnt {
@@ -49,14 +51,29 @@ struct LvEnt {
   double w;
 };
 
+// One level as the kernel reads it (passed by value: constant bank).  Accumulated targets use a
+// DENSE weight table wt[(i * (K + 1) + k) * tgn + q] (zero where input i, degree k does not feed
+// target q), so the kernel's loops over degrees and targets are compile-time and an entry costs
+// one complex FMA with a uniform operand -- no per-entry decoding.  Child vectors with a single
+// term are written directly (`direct`), which keeps the accumulator count small.
+struct LvDirect {
+  short slot;
+  signed char k;
+  double w;
+};
 struct LvLevel {
   int axis;
   int K;
   int nin, ntg;
+  int tgn;                  // accumulators of the kernel instantiation (1, 2, 4, 8, 16): stride of wt
   short in_buf[LV_MAXIN];   // -2 = v, >= 0 slot
   short tg_buf[LV_MAXTG];   // -1 = y, >= 0 slot
-  short ik_start[LV_MAXIN * (LV_MAXK + 1) + 1];  // entries of (input i, degree k) at [i*(K+1)+k]
-  LvEnt ent[LV_MAXENT];     // grouped by input: T_0..T_K of an input are computed once
+  unsigned short in_pmask[LV_MAXIN];  // window positions (bit p = offset p - K) the entries of input i read
+  unsigned char in_kmask[LV_MAXIN];   // degrees k of input i that feed accumulated targets
+  unsigned char in_dmask[LV_MAXIN];   // degrees k of input i with directly written children
+  short d_start[LV_MAXIN + 1];        // direct entries of input i: direct[d_start[i] .. d_start[i + 1])
+  LvDirect direct[LV_MAXDIRECT];
+  double wt[LV_WT];
 };
 
 struct LvProgram {
@@ -75,6 +92,7 @@ struct Builder {
   std::map<int, int> in_index;                        // buffer -> input index
   std::map<int, std::vector<std::pair<int, LvEnt>>> tg;  // target buffer -> (order, entry)
   bool ok = true;
+  int nent = 0;
   int input(int buf) {
     auto it = in_index.find(buf);
     if (it != in_index.end()) return it->second;
@@ -114,19 +132,27 @@ struct Builder {
       ++L.ntg;
     }
     if ((int)all.size() > LV_MAXENT) return false;
-    std::stable_sort(all.begin(), all.end(), [](const LvEnt& a, const LvEnt& b) {
-      return a.input != b.input ? a.input < b.input : a.k < b.k;
-    });
-    int ne = 0;
-    for (int i = 0; i < L.nin; ++i)
-      for (int k = 0; k <= LV_MAXK; ++k) {
-        L.ik_start[i * (LV_MAXK + 1) + k] = (short)ne;
-        while (ne < (int)all.size() && all[ne].input == i && all[ne].k == k) {
-          L.ent[ne] = all[ne];
-          ++ne;
-        }
+    L.tgn = L.ntg <= 1 ? 1 : L.ntg <= 2 ? 2 : L.ntg <= 4 ? 4 : L.ntg <= 8 ? 8 : LV_MAXTG;
+    if (L.nin * (L.K + 1) * L.tgn > LV_WT) return false;
+    for (int i = 0; i < L.nin * (L.K + 1) * L.tgn; ++i) L.wt[i] = 0.0;
+    for (int i = 0; i < L.nin; ++i) L.in_pmask[i] = 0, L.in_kmask[i] = 0, L.in_dmask[i] = 0;
+    std::stable_sort(all.begin(), all.end(), [](const LvEnt& a, const LvEnt& b) { return a.input < b.input; });
+    int nd = 0, cur = 0;
+    for (const LvEnt& e : all) {
+      while (cur <= e.input) L.d_start[cur++] = (short)nd;
+      // T_k reads the offsets d = -k, -k + 2, .., k of the level's window
+      for (int d = -e.k; d <= e.k; d += 2) L.in_pmask[e.input] |= (unsigned short)(1u << (L.K + d));
+      if (e.tg == 0xFF) {
+        if (nd >= LV_MAXDIRECT) return false;
+        L.direct[nd++] = {e.slot, e.k, e.w};
+        L.in_dmask[e.input] |= (unsigned char)(1u << e.k);
+      } else {
+        L.wt[(e.input * (L.K + 1) + e.k) * L.tgn + e.tg] += e.w;
+        L.in_kmask[e.input] |= (unsigned char)(1u << e.k);
       }
-    L.ik_start[L.nin * (LV_MAXK + 1)] = (short)ne;
+    }
+    while (cur <= L.nin) L.d_start[cur++] = (short)nd;
+    nent = (int)all.size();
     return true;
   }
 };
@@ -334,8 +360,8 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut,
 static void dump_plan(const LvProgram& P) {  // HP_LEVEL_DEBUG=1: planner output on stderr
   fprintf(stderr, "[hp_level] %zu levels, %d slots, cost %.2f\n", P.levels.size(), P.nslots, P.cost);
   for (const LvLevel& L : P.levels) {
-    fprintf(stderr, "  axis %d K %d inputs %d targets %d entries %d\n", L.axis, L.K, L.nin, L.ntg,
-            (int)L.ik_start[L.nin * (LV_MAXK + 1)]);
+    fprintf(stderr, "  axis %d K %d inputs %d targets %d accumulators*100+direct %d\n", L.axis, L.K, L.nin, L.ntg,
+            L.tgn * 100 + (int)L.d_start[L.nin]);
   }
 }
 
@@ -397,7 +423,8 @@ __global__ void __launch_bounds__(256, LV_MINB) k_level(int64_t n, int64_t batch
                                                double inv_L, double two_L, const double2* __restrict__ v,
                                                double2* __restrict__ slots, double2* __restrict__ y, int first,
                                                int osc, double2* __restrict__ dotp,
-                                               const int32_t* __restrict__ perm) {
+                                               const int32_t* __restrict__ perm,
+                                               const double* __restrict__ sqtab) {
   constexpr int S = 2 * K + 1;
   double2 dacc = make_double2(0.0, 0.0);
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
@@ -418,14 +445,35 @@ __global__ void __launch_bounds__(256, LV_MINB) k_level(int64_t n, int64_t batch
     int64_t seg[S];
     int jo;
     ax.template segment_pre<K>(pre_o, o, jo, seg);
-    // ladder coefficients of the window, sq[p] = sqrt(j_p / 2) (cd at p, cu at p - 1); positions
-    // with j < 0 are absent (forced to zero below).  Computed, not tabled: a table load would sit
-    // on the dependent chain behind the j load (measured slower on cfg3)
-    double sq[S + 1];
+    // links of the window: lk[p] = sqrt(j_p / 2) couples positions p - 1 and p (cd at p = cu at
+    // p - 1); a link with an absent end is 0, which is the restriction of the ladder to the set
+    double lk[S + 1];
 #pragma unroll
-    for (int p = 0; p <= S; ++p) {
+    for (int p = 1; p < S; ++p) {
       const int j = jo + p - K;
-      sq[p] = j > 0 ? sqrt(j * 0.5) : 0.0;
+      lk[p] = (seg[p - 1] >= 0 && seg[p] >= 0) ? (sqtab ? __ldg(sqtab + j) : sqrt(j * 0.5)) : 0.0;
+    }
+    // band rows R_k[p] = [T_k(X_a / L)]_{o, o + (p - K) e_a} of the restricted operator, by the
+    // three-term recurrence on the row vector (the operator is symmetric); T_k couples only
+    // offsets d = p - K with |d| <= k and d = k mod 2.  Formed once per ordinal and shared by
+    // every input vector and batch member: an input costs k + 1 complex FMAs per degree.
+    double R[K + 1][S];
+#pragma unroll
+    for (int k = 1; k <= K; ++k) {
+      const double sc = k == 1 ? inv_L : two_L;
+#pragma unroll
+      for (int p = 0; p < S; ++p) {
+        const int d = p - K;
+        if (d < -k || d > k || ((d + k) & 1)) continue;
+        double a = 0.0;
+        // (R_{k-1} J)[p] = R_{k-1}[p-1] lk[p] + R_{k-1}[p+1] lk[p+1]
+        if (d - 1 >= -(k - 1)) a = (k == 1 ? 1.0 : R[k - 1][p - 1]) * lk[p];
+        if (d + 1 <= k - 1) a = (d - 1 >= -(k - 1)) ? fma(k == 1 ? 1.0 : R[k - 1][p + 1], lk[p + 1], a)
+                                                    : (k == 1 ? 1.0 : R[k - 1][p + 1]) * lk[p + 1];
+        a *= sc;
+        if (k >= 2 && d >= -(k - 2) && d <= k - 2) a -= (k == 2 ? 1.0 : R[k - 2][p]);
+        R[k][p] = a;
+      }
     }
     double lev = 0.0;
     if (osc)
@@ -436,55 +484,42 @@ __global__ void __launch_bounds__(256, LV_MINB) k_level(int64_t n, int64_t batch
 #pragma unroll
       for (int q = 0; q < TGN; ++q) accs[q] = make_double2(0.0, 0.0);
       for (int ii = 0; ii < lv.nin; ++ii) {
-        // T_0..T_K of this input at o, once
         const int ib = lv.in_buf[ii];
         const double2* x = ib == -2 ? v + bo : slots + (int64_t)ib * n * batch + bo;
-        // entries of this input at degree kk receive t (static indices only: no local memory)
-        auto emit = [&](int kk, double2 t) {
-          const int e0 = lv.ik_start[ii * (LV_MAXK + 1) + kk], e1 = lv.ik_start[ii * (LV_MAXK + 1) + kk + 1];
-          for (int e = e0; e < e1; ++e) {
-            const LvEnt E = lv.ent[e];
-            if (E.tg == 0xFF) {
-              slots[(int64_t)E.slot * n * batch + bo + o] = make_double2(E.w * t.x, E.w * t.y);
-              continue;
-            }
-#pragma unroll
-            for (int q = 0; q < TGN; ++q)
-              if (E.tg == q) {
-                accs[q].x = fma(E.w, t.x, accs[q].x);
-                accs[q].y = fma(E.w, t.y, accs[q].y);
-              }
-          }
-        };
-        double2 Tm[S], Tc[S], Tn[S];
+        const unsigned need = lv.in_pmask[ii];  // window positions some entry of this input reads
+        const unsigned km = lv.in_kmask[ii], dm = lv.in_dmask[ii];
+        double2 xw[S];
 #pragma unroll
         for (int p = 0; p < S; ++p) {
           HP_DCHECK(seg[p] < n);
-          Tm[p] = seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
+          xw[p] = ((need >> p) & 1u) && seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
         }
-        emit(0, Tm[K]);
 #pragma unroll
-        for (int k = 1; k <= K; ++k) {
-          const double sc = k == 1 ? inv_L : two_L;
+        for (int k = 0; k <= K; ++k) {
+          if (!(((km | dm) >> k) & 1u)) continue;  // uniform: no entry of (input, degree)
+          double2 tk = make_double2(0.0, 0.0);
+          if (k == 0) tk = xw[K];
 #pragma unroll
-          for (int p = k; p < S - k; ++p) {
-            const double2 lo = k == 1 ? Tm[p - 1] : Tc[p - 1];
-            const double2 hi = k == 1 ? Tm[p + 1] : Tc[p + 1];
-            double2 r = make_double2(sc * fma(sq[p], lo.x, sq[p + 1] * hi.x), sc * fma(sq[p], lo.y, sq[p + 1] * hi.y));
-            if (k > 1) {
-              r.x -= Tm[p].x;
-              r.y -= Tm[p].y;
+          for (int p = 0; p < S; ++p) {
+            const int d = p - K;
+            if (k == 0 || d < -k || d > k || ((d + k) & 1)) continue;
+            tk.x = fma(R[k][p], xw[p].x, tk.x);
+            tk.y = fma(R[k][p], xw[p].y, tk.y);
+          }
+          if ((km >> k) & 1u) {
+#pragma unroll
+            for (int q = 0; q < TGN; ++q) {
+              const double w = lv.wt[(ii * (K + 1) + k) * TGN + q];
+              accs[q].x = fma(w, tk.x, accs[q].x);
+              accs[q].y = fma(w, tk.y, accs[q].y);
             }
-            if (seg[p] < 0) r = make_double2(0.0, 0.0);
-            Tn[p] = r;
           }
-          if (k > 1) {
-#pragma unroll
-            for (int p = 0; p < S; ++p) Tm[p] = Tc[p];
-          }
-#pragma unroll
-          for (int p = 0; p < S; ++p) Tc[p] = Tn[p];
-          emit(k, Tc[K]);
+          if ((dm >> k) & 1u)
+            for (int e = lv.d_start[ii]; e < lv.d_start[ii + 1]; ++e)
+              if (lv.direct[e].k == k) {
+                const double w = lv.direct[e].w;
+                slots[(int64_t)lv.direct[e].slot * n * batch + bo + o] = make_double2(w * tk.x, w * tk.y);
+              }
         }
       }
 #pragma unroll
@@ -579,75 +614,86 @@ static hp_status window_table(const hp_set_s* s, int a, int K, cudaStream_t st, 
   return HP_OK;
 }
 
+// the instantiation whose accumulator count matches the level's dense weight table
+template <int K, class AX, class AXS>
+static void launch_tgn(int grid, cudaStream_t st, int64_t n, int64_t batch, const AX& ax, const AXS& axs, int dim,
+                       const LvLevel& lv, double L, const double2* v, double2* slots, double2* y, int first,
+                       int osc, double2* dotp, const int32_t* perm, const double* sqtab) {
+#define HP_LV_GO(T)                                                                                          \
+  k_level<K, T, AX, AXS><<<grid, 256, 0, st>>>(n, batch, ax, axs, dim, lv, 1.0 / L, 2.0 / L, v, slots, y, \
+                                                 first, osc, dotp, perm, sqtab)
+  switch (lv.tgn) {
+    case 1: HP_LV_GO(1); break;
+    case 2: HP_LV_GO(2); break;
+    case 4: HP_LV_GO(4); break;
+    case 8: HP_LV_GO(8); break;
+    default: HP_LV_GO(LV_MAXTG); break;
+  }
+#undef HP_LV_GO
+}
+
 template <int K>
 static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, const double2* v, double2* slots,
                               double2* y, int64_t batch, int first, int osc, double2* dotp, int grid,
-                              cudaStream_t st, const int32_t* perm) {
+                              cudaStream_t st, const int32_t* perm, const double* sqtab) {
   const int64_t n = s->n;
   if (s->boxed) {
     LvAllBox axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->box(a);
-    if (lv.ntg <= 1)
-      k_level<K, 1, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv, 1.0 / L,
-                                                          2.0 / L, v, slots, y, first, osc, dotp, perm);
-    else if (lv.ntg <= 4)
-      k_level<K, 4, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv, 1.0 / L,
-                                                          2.0 / L, v, slots, y, first, osc, dotp, perm);
-    else
-      k_level<K, LV_MAXTG, AxBox, LvAllBox><<<grid, 256, 0, st>>>(n, batch, s->box(lv.axis), axs, s->dim, lv,
-                                                                 1.0 / L, 2.0 / L, v, slots, y, first, osc, dotp, perm);
+    launch_tgn<K>(grid, st, n, batch, s->box(lv.axis), axs, s->dim, lv, L, v, slots, y, first, osc, dotp, perm, sqtab);
   } else {
     LvAllTab axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
     int kwin = 0;
-    // innermost axis of a hyperbolic cross (downward closed, lexicographic): windows from the j table
+    const int32_t* win = nullptr;
     if (lv.axis == s->dim - 1 && !perm && s->kind == HP_KIND_HYPERBOLIC) {
-      const AxInner ax(s->tab(lv.axis), n);
-      if (lv.ntg <= 1)
-        k_level<K, 1, AxInner, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
-                                                              slots, y, first, osc, dotp, perm);
-      else if (lv.ntg <= 4)
-        k_level<K, 4, AxInner, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
-                                                              slots, y, first, osc, dotp, perm);
-      else
-        k_level<K, LV_MAXTG, AxInner, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L,
-                                                                     2.0 / L, v, slots, y, first, osc, dotp, perm);
-    } else if (const int32_t* win = nullptr;
-               batch > 1 && window_table(s, lv.axis, K, st, &win, &kwin) == HP_OK && win) {
+      // innermost axis of a hyperbolic cross (downward closed, lexicographic): windows from the j table
+      launch_tgn<K>(grid, st, n, batch, AxInner(s->tab(lv.axis), n), axs, s->dim, lv, L, v, slots, y, first, osc,
+                    dotp, perm, sqtab);
+    } else if (batch > 1 && window_table(s, lv.axis, K, st, &win, &kwin) == HP_OK && win) {
       // batched levels read precomputed windows (cfg5 713 -> 696 ms); single vectors walk the tables
       // with the first hop prefetched (cfg3: 5.86 ms vs 6.03 with windows; profiles/r2/sweep_level.txt)
-      const AxWin ax(s->tab(lv.axis), win, n, kwin);
-      if (lv.ntg <= 1)
-        k_level<K, 1, AxWin, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
-                                                            slots, y, first, osc, dotp, perm);
-      else if (lv.ntg <= 4)
-        k_level<K, 4, AxWin, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
-                                                            slots, y, first, osc, dotp, perm);
-      else
-        k_level<K, LV_MAXTG, AxWin, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L,
-                                                                   2.0 / L, v, slots, y, first, osc, dotp, perm);
+      launch_tgn<K>(grid, st, n, batch, AxWin(s->tab(lv.axis), win, n, kwin), axs, s->dim, lv, L, v, slots, y,
+                    first, osc, dotp, perm, sqtab);
     } else if (batch == 1) {
-      const AxTabPf ax(s->tab(lv.axis));
-      if (lv.ntg <= 1)
-        k_level<K, 1, AxTabPf, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
-                                                              slots, y, first, osc, dotp, perm);
-      else if (lv.ntg <= 4)
-        k_level<K, 4, AxTabPf, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L, 2.0 / L, v,
-                                                              slots, y, first, osc, dotp, perm);
-      else
-        k_level<K, LV_MAXTG, AxTabPf, LvAllTab><<<grid, 256, 0, st>>>(n, batch, ax, axs, s->dim, lv, 1.0 / L,
-                                                                     2.0 / L, v, slots, y, first, osc, dotp, perm);
-    } else if (lv.ntg <= 1)
-      k_level<K, 1, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv, 1.0 / L,
-                                                          2.0 / L, v, slots, y, first, osc, dotp, perm);
-    else if (lv.ntg <= 4)
-      k_level<K, 4, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv, 1.0 / L,
-                                                          2.0 / L, v, slots, y, first, osc, dotp, perm);
-    else
-      k_level<K, LV_MAXTG, AxTab, LvAllTab><<<grid, 256, 0, st>>>(n, batch, s->tab(lv.axis), axs, s->dim, lv,
-                                                                 1.0 / L, 2.0 / L, v, slots, y, first, osc, dotp, perm);
+      launch_tgn<K>(grid, st, n, batch, AxTabPf(s->tab(lv.axis)), axs, s->dim, lv, L, v, slots, y, first, osc,
+                    dotp, perm, sqtab);
+    } else {
+      launch_tgn<K>(grid, st, n, batch, s->tab(lv.axis), axs, s->dim, lv, L, v, slots, y, first, osc, dotp, perm,
+                    sqtab);
+    }
   }
   HP_LAUNCH_CHECK("k_level");
+  return HP_OK;
+}
+
+// ---------------------------------------------------------------- ladder coefficients
+
+__global__ void k_ladder_table(int m, double* __restrict__ t) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    t[i] = i > 8 ? sqrt((i - 8) * 0.5) : 0.0;
+}
+
+// sqrt(j / 2) tabulated once per set (pointer to the entry of j = 0), so the level kernels load
+// their 2K window links instead of evaluating 2K double-precision square roots per ordinal.
+// Sets whose indices may exceed `bound` (explicit lists) get no table (the kernels call sqrt).
+static hp_status ladder_table(const hp_set_s* s, cudaStream_t st, const double** out) {
+  *out = nullptr;
+  static const int on = [] {
+    const char* e = getenv("HP_LEVEL_SQTAB");
+    return e ? atoi(e) : 1;
+  }();
+  if (!on || s->kind == HP_KIND_CUSTOM) return HP_OK;
+  std::lock_guard<std::mutex> g(s->perm_mtx);
+  if (!s->d_sqtab) {
+    const int m = s->bound + 17;
+    double* t = nullptr;
+    HP_CUDA(cudaMalloc(&t, (size_t)m * sizeof(double)));
+    k_ladder_table<<<grid_for(m, 256), 256, 0, st>>>(m, t);
+    HP_LAUNCH_CHECK("k_ladder_table");
+    s->d_sqtab = t;
+  }
+  *out = s->d_sqtab + 8;
   return HP_OK;
 }
 
@@ -809,6 +855,8 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
         last_y = li;
       }
   if (first_y < 0) return HP_OK;
+  const double* sqtab = nullptr;
+  if (hp_status rc = ladder_table(s, st, &sqtab)) return rc;
   for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
     const int64_t nb = std::min(chunk, batch - b0);
     const double2* v = (const double2*)in + b0 * n;
@@ -824,11 +872,11 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
       if (rc) return rc;
       const int oscf = last && osc ? 1 : 0;
       switch (lv.K) {
-        case 0: rc = launch_level<0>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
-        case 1: rc = launch_level<1>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
-        case 2: rc = launch_level<2>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
-        case 3: rc = launch_level<3>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
-        default: rc = launch_level<4>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm); break;
+        case 0: rc = launch_level<0>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm, sqtab); break;
+        case 1: rc = launch_level<1>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm, sqtab); break;
+        case 2: rc = launch_level<2>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm, sqtab); break;
+        case 3: rc = launch_level<3>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm, sqtab); break;
+        default: rc = launch_level<4>(s, lv, halfwidth, v, slots, y, nb, first, oscf, dotp, grid, st, perm, sqtab); break;
       }
       if (rc) return rc;
       if (dotp) dot->n = grid;
