@@ -413,11 +413,11 @@ static std::shared_ptr<const LvProgram> cached_plan(int dim, const std::vector<T
 
 template <int K, int TGN, class AX, class AXS>
 #ifndef LV_MINB
-// minimum resident 256-thread blocks per SM handed to ptxas: 4 (<= 64 registers) for the K = 3
-// levels, ptxas's own choice elsewhere.  Measured (profiles/r2/sweep_level.txt): capping every
-// level at 4 blocks made cfg5 697 -> 668 ms but cfg3 (K = 2) 5.86 -> 6.47 and cfg2 (K = 4)
-// 0.092 -> 0.107 ms; 2 or 3 blocks were slower everywhere
-#define LV_MINB (K == 3 ? 4 : 0)
+// minimum resident 256-thread blocks per SM handed to ptxas: 4 (<= 64 registers).  Occupancy beats
+// spill traffic on these gather kernels (profiles/r2/sweep_level.txt, dense-weight kernels: cfg3
+// 6.00 ms uncapped (76 registers), 5.13 at 4 blocks, 6.04 at 5, 7.11 at 6; cfg5 654 / 511 / 699 /
+// 874 ms)
+#define LV_MINB 4
 #endif
 __global__ void __launch_bounds__(256, LV_MINB) k_level(int64_t n, int64_t batch, AX ax, AXS axs, int dim, LvLevel lv,
                                                double inv_L, double two_L, const double2* __restrict__ v,
