@@ -16,8 +16,8 @@
 #include <vector>
 
 #include "../../include/hprop_b200.h"
+#include "hp_device.cuh"
 
-#define HP_MAXDIM 16
 #define HP_ABI 1
 
 namespace hp {
@@ -41,24 +41,6 @@ hp_status cuda_fail(cudaError_t e, const char* what);
     cudaError_t e_ = cudaGetLastError();                \
     if (e_ != cudaSuccess) return hp::cuda_fail(e_, what); \
   } while (0)
-
-// Device-side bounds checks (compute-sanitizer is unavailable on this pool): compiled into the
-// `make checks` variant (libhprop_b200_checks.so, -DHP_DEVICE_CHECKS) only; a failed check traps,
-// which surfaces as a sticky CUDA error in the calling test.
-#ifdef HP_DEVICE_CHECKS
-#define HP_DCHECK(cond)                                                                          \
-  do {                                                                                           \
-    if (!(cond)) {                                                                               \
-      printf("HP_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,      \
-             (int)blockIdx.x, (int)threadIdx.x);                                                 \
-      __trap();                                                                                  \
-    }                                                                                            \
-  } while (0)
-#else
-#define HP_DCHECK(cond) \
-  do {                  \
-  } while (0)
-#endif
 
 // NVTX range around a C-ABI entry point (visible in Nsight timelines; a no-op without a tool
 // attached).  NVTX v3 is header-only.
@@ -123,150 +105,6 @@ __device__ __forceinline__ bool sfinite(double2 x) { return isfinite(x.x) && isf
 
 template <class T>
 __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
-
-// ---------------------------------------------------------------- axis views
-// A view answers, for one axis and one ordinal: the (global) order j_l used
-// in the ladder coefficients and the ordinals of the -/+ neighbours (-1 if
-// absent).  Boxes (full cubes and j1-slabs of full cubes) use stride
-// arithmetic; every other set uses device neighbour tables.
-struct AxBox {
-  int64_t stride;  // ordinal stride of this axis
-  int side;        // local extent of this axis
-  int joff;        // global offset of local j (slab shards, axis 1 only)
-  __device__ __forceinline__ int jloc(int64_t o) const { return (int)((o / stride) % side); }
-  __device__ __forceinline__ void at(int64_t o, int& j, int64_t& dn, int64_t& up) const {
-    int jl = jloc(o);
-    j = jl + joff;
-    dn = jl > 0 ? o - stride : -1;
-    up = jl < side - 1 ? o + stride : -1;
-  }
-  __device__ __forceinline__ int64_t dn_of(int64_t o) const { return jloc(o) > 0 ? o - stride : -1; }
-  __device__ __forceinline__ int64_t up_of(int64_t o) const { return jloc(o) < side - 1 ? o + stride : -1; }
-  // the axis line through o out to +-K: seg[K + d] = ordinal of j + d e, or -1 (one division)
-  template <int K>
-  __device__ __forceinline__ void segment(int64_t o, int& j, int64_t* seg) const {
-    const int jl = o < (int64_t)0x7fffffff ? (int)(((unsigned)o / (unsigned)stride) % (unsigned)side) : jloc(o);
-    j = jl + joff;
-#pragma unroll
-    for (int d = -K; d <= K; ++d) seg[K + d] = (jl + d >= 0 && jl + d < side) ? o + d * stride : -1;
-  }
-  // nothing to prefetch: stride arithmetic
-  struct Pre {};
-  __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
-    segment<K>(o, j, seg);
-  }
-};
-
-struct AxTab {
-  const int32_t* down;
-  const int32_t* up;
-  const int32_t* jv;
-  __device__ __forceinline__ void at(int64_t o, int& j, int64_t& dn, int64_t& up_) const {
-    j = __ldg(jv + o);
-    dn = __ldg(down + o);
-    up_ = __ldg(up + o);
-  }
-  __device__ __forceinline__ int64_t dn_of(int64_t o) const { return __ldg(down + o); }
-  __device__ __forceinline__ int64_t up_of(int64_t o) const { return __ldg(up + o); }
-  // the axis line through o out to +-K via the tables (down chains never break in a
-  // downward-closed set; up chains stop at the first pruned index)
-  template <int K>
-  __device__ __forceinline__ void segment(int64_t o, int& j, int64_t* seg) const {
-    int64_t dn, up_;
-    at(o, j, dn, up_);
-    seg[K] = o;
-    if (K > 0) {
-      seg[K - 1] = dn;
-      seg[K + 1] = up_;
-    }
-#pragma unroll
-    for (int d = 2; d <= K; ++d) {
-      seg[K - d] = seg[K - d + 1] >= 0 ? dn_of(seg[K - d + 1]) : -1;
-      seg[K + d] = seg[K + d - 1] >= 0 ? up_of(seg[K + d - 1]) : -1;
-    }
-  }
-  // no prefetch (batched levels: the walk is shared by the batch's vectors already)
-  struct Pre {};
-  __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
-    segment<K>(o, j, seg);
-  }
-};
-
-// The innermost axis of a tabled (lexicographic, downward-closed) set: its lines are contiguous
-// ordinal runs starting at j = 0, so j - d e_N is o - d whenever j >= d, and o + d lies on the
-// same line iff its own j equals j + d (the next line restarts at 0).  The window is formed from
-// the j table alone -- K + 1 independent, coalesced loads instead of the dependent down/up walk.
-struct AxInner : AxTab {
-  AxInner() = default;
-  explicit AxInner(const AxTab& t, int64_t n_) : AxTab(t), n(n_) {}
-  int64_t n;
-  struct Pre {};
-  __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
-    j = __ldg(jv + o);
-    seg[K] = o;
-#pragma unroll
-    for (int d = 1; d <= K; ++d) {
-      seg[K - d] = j >= d ? o - d : -1;
-      seg[K + d] = (o + d < n && __ldg(jv + o + d) == j + d) ? o + d : -1;
-    }
-  }
-};
-
-// Precomputed windows (hp_level.cu window_table): row r < K holds the ordinal of j - (K - r) e_a,
-// row r >= K that of j + (r - K + 1) e_a (-1 absent), so a level reads 2K independent coalesced
-// ordinals instead of walking the down / up chains (whose second hops are scattered 4-byte reads).
-struct AxWin : AxTab {
-  AxWin() = default;
-  AxWin(const AxTab& t, const int32_t* w, int64_t n_, int kw) : AxTab(t), win(w), n(n_), kwin(kw) {}
-  const int32_t* win;
-  int64_t n;
-  int kwin;  // K of the stored table (>= the level's K)
-  struct Pre {};
-  __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
-    j = __ldg(jv + o);
-    seg[K] = o;
-#pragma unroll
-    for (int d = 1; d <= K; ++d) {
-      seg[K - d] = __ldg(win + (int64_t)(kwin - d) * n + o);
-      seg[K + d] = __ldg(win + (int64_t)(kwin + d - 1) * n + o);
-    }
-  }
-};
-
-// AxTab whose first walk hop is loaded one grid-stride iteration ahead (software pipelining of the
-// dependent table chain: j / down / up of the next ordinal are in flight while the current one's
-// windows are gathered).  Single-vector levels: cfg3 6.24 -> 5.91 ms; a batch of 4 slowed 1%.
-struct AxTabPf : AxTab {
-  AxTabPf() = default;
-  explicit AxTabPf(const AxTab& t) : AxTab(t) {}
-  struct Pre {
-    int j;
-    int32_t dn, up;
-  };
-  __device__ __forceinline__ Pre pre(int64_t o) const { return {__ldg(jv + o), __ldg(down + o), __ldg(up + o)}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre& p, int64_t o, int& j, int64_t* seg) const {
-    j = p.j;
-    seg[K] = o;
-    if (K > 0) {
-      seg[K - 1] = p.dn;
-      seg[K + 1] = p.up;
-    }
-#pragma unroll
-    for (int d = 2; d <= K; ++d) {
-      seg[K - d] = seg[K - d + 1] >= 0 ? dn_of(seg[K - d + 1]) : -1;
-      seg[K + d] = seg[K + d - 1] >= 0 ? up_of(seg[K + d - 1]) : -1;
-    }
-  }
-};
 
 }  // namespace hp
 

@@ -36,46 +36,6 @@
 
 namespace hp {
 
-constexpr int LV_MAXIN = 64;
-constexpr int LV_MAXTG = 16;  // targets accumulate in registers
-constexpr int LV_MAXENT = 160;
-constexpr int LV_MAXDIRECT = 48;
-constexpr int LV_WT = 640;  // dense weights: nin * (K + 1) * tgn doubles
-constexpr int LV_MAXK = 4;
-
-struct LvEnt {
-  unsigned char input;  // index into in_buf
-  unsigned char tg;     // index into tg_buf (accumulated target), or 0xFF: write w * T_k to `slot`
-  signed char k;        // degree
-  short slot;
-  double w;
-};
-
-// One level as the kernel reads it (passed by value: constant bank).  Accumulated targets use a
-// DENSE weight table wt[(i * (K + 1) + k) * tgn + q] (zero where input i, degree k does not feed
-// target q), so the kernel's loops over degrees and targets are compile-time and an entry costs
-// one complex FMA with a uniform operand -- no per-entry decoding.  Child vectors with a single
-// term are written directly (`direct`), which keeps the accumulator count small.
-struct LvDirect {
-  short slot;
-  signed char k;
-  double w;
-};
-struct LvLevel {
-  int axis;
-  int K;
-  int nin, ntg;
-  int tgn;                  // accumulators of the kernel instantiation (1, 2, 4, 8, 16): stride of wt
-  short in_buf[LV_MAXIN];   // -2 = v, >= 0 slot
-  short tg_buf[LV_MAXTG];   // -1 = y, >= 0 slot
-  unsigned short in_pmask[LV_MAXIN];  // window positions (bit p = offset p - K) the entries of input i read
-  unsigned char in_kmask[LV_MAXIN];   // degrees k of input i that feed accumulated targets
-  unsigned char in_dmask[LV_MAXIN];   // degrees k of input i with directly written children
-  short d_start[LV_MAXIN + 1];        // direct entries of input i: direct[d_start[i] .. d_start[i + 1])
-  LvDirect direct[LV_MAXDIRECT];
-  double wt[LV_WT];
-};
-
 struct LvProgram {
   std::vector<LvLevel> levels;
   int nslots = 0;
@@ -409,158 +369,6 @@ static std::shared_ptr<const LvProgram> cached_plan(int dim, const std::vector<T
   return P;
 }
 
-// ---------------------------------------------------------------- kernel
-
-template <int K, int TGN, class AX, class AXS>
-#ifndef LV_MINB
-// minimum resident 256-thread blocks per SM handed to ptxas: 4 (<= 64 registers).  Occupancy beats
-// spill traffic on these gather kernels (profiles/r2/sweep_level.txt, dense-weight kernels: cfg3
-// 6.00 ms uncapped (76 registers), 5.13 at 4 blocks, 6.04 at 5, 7.11 at 6; cfg5 654 / 511 / 699 /
-// 874 ms)
-#define LV_MINB 4
-#endif
-__global__ void __launch_bounds__(256, LV_MINB) k_level(int64_t n, int64_t batch, AX ax, AXS axs, int dim, LvLevel lv,
-                                               double inv_L, double two_L, const double2* __restrict__ v,
-                                               double2* __restrict__ slots, double2* __restrict__ y, int first,
-                                               int osc, double2* __restrict__ dotp,
-                                               const int32_t* __restrict__ perm,
-                                               const double* __restrict__ sqtab) {
-  constexpr int S = 2 * K + 1;
-  double2 dacc = make_double2(0.0, 0.0);
-  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  // perm (outer axes of tabled sets): line-blocked order (line_order below), so the +-K
-  // windows of neighbouring warps overlap in L1/L2 (ordinal order puts the window positions
-  // one sub-block apart, far beyond L2 reuse)
-  int64_t o_next = t < n ? (perm ? (int64_t)__ldg(perm + t) : t) : 0;
-  typename AX::Pre pre_next = ax.pre(o_next);
-  for (; t < n; t += gstride) {
-    const int64_t o = o_next;
-    const typename AX::Pre pre_o = pre_next;
-    if (t + gstride < n) {  // the next ordinal's first walk hop, in flight during this one
-      o_next = perm ? (int64_t)__ldg(perm + t + gstride) : t + gstride;
-      pre_next = ax.pre(o_next);
-    }
-    // the axis line through o: seg[K + d] = ordinal of j + d e_a, or -1
-    int64_t seg[S];
-    int jo;
-    ax.template segment_pre<K>(pre_o, o, jo, seg);
-    // links of the window: lk[p] = sqrt(j_p / 2) couples positions p - 1 and p (cd at p = cu at
-    // p - 1); a link with an absent end is 0, which is the restriction of the ladder to the set
-    double lk[S + 1];
-#pragma unroll
-    for (int p = 1; p < S; ++p) {
-      const int j = jo + p - K;
-      lk[p] = (seg[p - 1] >= 0 && seg[p] >= 0) ? (sqtab ? __ldg(sqtab + j) : sqrt(j * 0.5)) : 0.0;
-    }
-    // band rows R_k[p] = [T_k(X_a / L)]_{o, o + (p - K) e_a} of the restricted operator, by the
-    // three-term recurrence on the row vector (the operator is symmetric); T_k couples only
-    // offsets d = p - K with |d| <= k and d = k mod 2.  Formed once per ordinal and shared by
-    // every input vector and batch member: an input costs k + 1 complex FMAs per degree.
-    double R[K + 1][S];
-#pragma unroll
-    for (int k = 1; k <= K; ++k) {
-      const double sc = k == 1 ? inv_L : two_L;
-#pragma unroll
-      for (int p = 0; p < S; ++p) {
-        const int d = p - K;
-        if (d < -k || d > k || ((d + k) & 1)) continue;
-        double a = 0.0;
-        // (R_{k-1} J)[p] = R_{k-1}[p-1] lk[p] + R_{k-1}[p+1] lk[p+1]
-        if (d - 1 >= -(k - 1)) a = (k == 1 ? 1.0 : R[k - 1][p - 1]) * lk[p];
-        if (d + 1 <= k - 1) a = (d - 1 >= -(k - 1)) ? fma(k == 1 ? 1.0 : R[k - 1][p + 1], lk[p + 1], a)
-                                                    : (k == 1 ? 1.0 : R[k - 1][p + 1]) * lk[p + 1];
-        a *= sc;
-        if (k >= 2 && d >= -(k - 2) && d <= k - 2) a -= (k == 2 ? 1.0 : R[k - 2][p]);
-        R[k][p] = a;
-      }
-    }
-    double lev = 0.0;
-    if (osc)
-      for (int a = 0; a < dim; ++a) lev += (double)axs.j(a, o) + 0.5;
-    for (int64_t b = 0; b < batch; ++b) {
-      const int64_t bo = b * n;
-      double2 accs[TGN];
-#pragma unroll
-      for (int q = 0; q < TGN; ++q) accs[q] = make_double2(0.0, 0.0);
-      for (int ii = 0; ii < lv.nin; ++ii) {
-        const int ib = lv.in_buf[ii];
-        const double2* x = ib == -2 ? v + bo : slots + (int64_t)ib * n * batch + bo;
-        const unsigned need = lv.in_pmask[ii];  // window positions some entry of this input reads
-        const unsigned km = lv.in_kmask[ii], dm = lv.in_dmask[ii];
-        double2 xw[S];
-#pragma unroll
-        for (int p = 0; p < S; ++p) {
-          HP_DCHECK(seg[p] < n);
-          xw[p] = ((need >> p) & 1u) && seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int k = 0; k <= K; ++k) {
-          if (!(((km | dm) >> k) & 1u)) continue;  // uniform: no entry of (input, degree)
-          double2 tk = make_double2(0.0, 0.0);
-          if (k == 0) tk = xw[K];
-#pragma unroll
-          for (int p = 0; p < S; ++p) {
-            const int d = p - K;
-            if (k == 0 || d < -k || d > k || ((d + k) & 1)) continue;
-            tk.x = fma(R[k][p], xw[p].x, tk.x);
-            tk.y = fma(R[k][p], xw[p].y, tk.y);
-          }
-          if ((km >> k) & 1u) {
-#pragma unroll
-            for (int q = 0; q < TGN; ++q) {
-              const double w = lv.wt[(ii * (K + 1) + k) * TGN + q];
-              accs[q].x = fma(w, tk.x, accs[q].x);
-              accs[q].y = fma(w, tk.y, accs[q].y);
-            }
-          }
-          if ((dm >> k) & 1u)
-            for (int e = lv.d_start[ii]; e < lv.d_start[ii + 1]; ++e)
-              if (lv.direct[e].k == k) {
-                const double w = lv.direct[e].w;
-                slots[(int64_t)lv.direct[e].slot * n * batch + bo + o] = make_double2(w * tk.x, w * tk.y);
-              }
-        }
-      }
-#pragma unroll
-      for (int tgi = 0; tgi < TGN; ++tgi) {
-        if (tgi >= lv.ntg) break;
-        double2 acc = accs[tgi];
-        const int tb = lv.tg_buf[tgi];
-        if (tb >= 0) {
-          slots[(int64_t)tb * n * batch + bo + o] = acc;
-        } else {
-          if (osc) {
-            double2 x = __ldg(v + bo + o);
-            acc.x = fma(lev, x.x, acc.x);
-            acc.y = fma(lev, x.y, acc.y);
-          }
-          if (!first) {
-            double2 old = y[bo + o];
-            acc.x += old.x;
-            acc.y += old.y;
-          }
-          y[bo + o] = acc;
-          if (dotp) cdot_acc(__ldg(v + bo + o), acc, dacc);
-        }
-      }
-    }
-  }
-  if (dotp) {
-    dacc = block_sum2(dacc);
-    if (threadIdx.x == 0) dotp[blockIdx.x] = dacc;
-  }
-}
-
-struct LvAllBox {
-  AxBox ax[HP_MAXDIM];
-  __device__ __forceinline__ int j(int a, int64_t o) const { return ax[a].jloc(o) + ax[a].joff; }
-};
-struct LvAllTab {
-  AxTab ax[HP_MAXDIM];
-  __device__ __forceinline__ int j(int a, int64_t o) const { return __ldg(ax[a].jv + o); }
-};
-
 // ---------------------------------------------------------------- precomputed windows
 
 template <int K>
@@ -614,13 +422,25 @@ static hp_status window_table(const hp_set_s* s, int a, int K, cudaStream_t st, 
   return HP_OK;
 }
 
-// the instantiation whose accumulator count matches the level's dense weight table
+// hp_level_jit.cu
+bool level_jit_enabled(int64_t work);
+bool level_jit_launch(int device, const char* ax_name, const void* ax, const char* axs_name, const void* axs,
+                      const LvLevel& lv, int grid, cudaStream_t st, int64_t n, int64_t batch, int dim, double inv_L,
+                      double two_L, const double2* v, double2* slots, double2* y, int first, int osc, double2* dotp,
+                      const int32_t* perm, const double* sqtab);
+
+// the specialised kernel of a large level if there is one, else the instantiation whose accumulator
+// count matches the level's dense weight table
 template <int K, class AX, class AXS>
-static void launch_tgn(int grid, cudaStream_t st, int64_t n, int64_t batch, const AX& ax, const AXS& axs, int dim,
+static void launch_tgn(int device, int grid, cudaStream_t st, int64_t n, int64_t batch, const AX& ax, const AXS& axs, int dim,
                        const LvLevel& lv, double L, const double2* v, double2* slots, double2* y, int first,
                        int osc, double2* dotp, const int32_t* perm, const double* sqtab) {
+  if (level_jit_enabled(n * batch) &&
+      level_jit_launch(device, AX::name(), &ax, AXS::name(), &axs, lv, grid, st, n, batch, dim, 1.0 / L, 2.0 / L, v, slots,
+                       y, first, osc, dotp, perm, sqtab))
+    return;
 #define HP_LV_GO(T)                                                                                          \
-  k_level<K, T, AX, AXS><<<grid, 256, 0, st>>>(n, batch, ax, axs, dim, lv, 1.0 / L, 2.0 / L, v, slots, y, \
+  k_level<K, T, AX, AXS, LvLevel><<<grid, 256, 0, st>>>(n, batch, ax, axs, dim, lv, 1.0 / L, 2.0 / L, v, slots, y, \
                                                  first, osc, dotp, perm, sqtab)
   switch (lv.tgn) {
     case 1: HP_LV_GO(1); break;
@@ -640,7 +460,7 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
   if (s->boxed) {
     LvAllBox axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->box(a);
-    launch_tgn<K>(grid, st, n, batch, s->box(lv.axis), axs, s->dim, lv, L, v, slots, y, first, osc, dotp, perm, sqtab);
+    launch_tgn<K>(s->device, grid, st, n, batch, s->box(lv.axis), axs, s->dim, lv, L, v, slots, y, first, osc, dotp, perm, sqtab);
   } else {
     LvAllTab axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
@@ -648,18 +468,18 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
     const int32_t* win = nullptr;
     if (lv.axis == s->dim - 1 && !perm && s->kind == HP_KIND_HYPERBOLIC) {
       // innermost axis of a hyperbolic cross (downward closed, lexicographic): windows from the j table
-      launch_tgn<K>(grid, st, n, batch, AxInner(s->tab(lv.axis), n), axs, s->dim, lv, L, v, slots, y, first, osc,
+      launch_tgn<K>(s->device, grid, st, n, batch, AxInner(s->tab(lv.axis), n), axs, s->dim, lv, L, v, slots, y, first, osc,
                     dotp, perm, sqtab);
     } else if (batch > 1 && window_table(s, lv.axis, K, st, &win, &kwin) == HP_OK && win) {
       // batched levels read precomputed windows (cfg5 713 -> 696 ms); single vectors walk the tables
       // with the first hop prefetched (cfg3: 5.86 ms vs 6.03 with windows; profiles/r2/sweep_level.txt)
-      launch_tgn<K>(grid, st, n, batch, AxWin(s->tab(lv.axis), win, n, kwin), axs, s->dim, lv, L, v, slots, y,
+      launch_tgn<K>(s->device, grid, st, n, batch, AxWin(s->tab(lv.axis), win, n, kwin), axs, s->dim, lv, L, v, slots, y,
                     first, osc, dotp, perm, sqtab);
     } else if (batch == 1) {
-      launch_tgn<K>(grid, st, n, batch, AxTabPf(s->tab(lv.axis)), axs, s->dim, lv, L, v, slots, y, first, osc,
+      launch_tgn<K>(s->device, grid, st, n, batch, AxTabPf(s->tab(lv.axis)), axs, s->dim, lv, L, v, slots, y, first, osc,
                     dotp, perm, sqtab);
     } else {
-      launch_tgn<K>(grid, st, n, batch, s->tab(lv.axis), axs, s->dim, lv, L, v, slots, y, first, osc, dotp, perm,
+      launch_tgn<K>(s->device, grid, st, n, batch, s->tab(lv.axis), axs, s->dim, lv, L, v, slots, y, first, osc, dotp, perm,
                     sqtab);
     }
   }

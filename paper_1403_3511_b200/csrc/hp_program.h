@@ -92,33 +92,4 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
                       const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
                       cudaStream_t st, bool* done, DotOut* dot = nullptr);
 
-// block-wide sum of a double2 (blockDim multiple of 32, <= 1024); result valid in thread 0
-__device__ __forceinline__ double2 block_sum2(double2 v) {
-  __shared__ double2 red_sh[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
-    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
-  }
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red_sh[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    int nw = (blockDim.x + 31) >> 5;
-    v = lane < nw ? red_sh[lane] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      v.x += __shfl_down_sync(0xffffffffu, v.x, o);
-      v.y += __shfl_down_sync(0xffffffffu, v.y, o);
-    }
-  }
-  return v;
-}
-// conj(a) * b accumulated into acc
-__device__ __forceinline__ void cdot_acc(double2 a, double2 b, double2& acc) {
-  acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
-  acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
-}
-
 }  // namespace hp
