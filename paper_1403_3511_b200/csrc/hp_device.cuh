@@ -43,6 +43,8 @@ namespace hp {
 // absent).  Boxes (full cubes and j1-slabs of full cubes) use stride
 // arithmetic; every other set uses device neighbour tables.
 struct AxBox {
+  typedef int64_t Idx;  // window ordinals of a box can exceed 32 bits
+  typedef int64_t UIdx;
 #ifndef __CUDACC_RTC__
   static const char* name() { return "hp::AxBox"; }  // type name in runtime-compiled source
 #endif
@@ -59,23 +61,25 @@ struct AxBox {
   __device__ __forceinline__ int64_t dn_of(int64_t o) const { return jloc(o) > 0 ? o - stride : -1; }
   __device__ __forceinline__ int64_t up_of(int64_t o) const { return jloc(o) < side - 1 ? o + stride : -1; }
   // the axis line through o out to +-K: seg[K + d] = ordinal of j + d e, or -1 (one division)
-  template <int K>
-  __device__ __forceinline__ void segment(int64_t o, int& j, int64_t* seg) const {
+  template <int K, class I>
+  __device__ __forceinline__ void segment(int64_t o, int& j, I* seg) const {
     const int jl = o < (int64_t)0x7fffffff ? (int)(((unsigned)o / (unsigned)stride) % (unsigned)side) : jloc(o);
     j = jl + joff;
 #pragma unroll
-    for (int d = -K; d <= K; ++d) seg[K + d] = (jl + d >= 0 && jl + d < side) ? o + d * stride : -1;
+    for (int d = -K; d <= K; ++d) seg[K + d] = (jl + d >= 0 && jl + d < side) ? (I)(o + d * stride) : (I)-1;
   }
   // nothing to prefetch: stride arithmetic
   struct Pre {};
   __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
+  template <int K, class I>
+  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, I* seg) const {
     segment<K>(o, j, seg);
   }
 };
 
 struct AxTab {
+  typedef uint32_t UIdx;
+  typedef int32_t Idx;  // tabled sets hold int32 ordinals: half the registers of the window
 #ifndef __CUDACC_RTC__
   static const char* name() { return "hp::AxTab"; }  // type name in runtime-compiled source
 #endif
@@ -91,26 +95,26 @@ struct AxTab {
   __device__ __forceinline__ int64_t up_of(int64_t o) const { return __ldg(up + o); }
   // the axis line through o out to +-K via the tables (down chains never break in a
   // downward-closed set; up chains stop at the first pruned index)
-  template <int K>
-  __device__ __forceinline__ void segment(int64_t o, int& j, int64_t* seg) const {
+  template <int K, class I>
+  __device__ __forceinline__ void segment(int64_t o, int& j, I* seg) const {
     int64_t dn, up_;
     at(o, j, dn, up_);
-    seg[K] = o;
+    seg[K] = (I)o;
     if (K > 0) {
-      seg[K - 1] = dn;
-      seg[K + 1] = up_;
+      seg[K - 1] = (I)dn;
+      seg[K + 1] = (I)up_;
     }
 #pragma unroll
     for (int d = 2; d <= K; ++d) {
-      seg[K - d] = seg[K - d + 1] >= 0 ? dn_of(seg[K - d + 1]) : -1;
-      seg[K + d] = seg[K + d - 1] >= 0 ? up_of(seg[K + d - 1]) : -1;
+      seg[K - d] = seg[K - d + 1] >= 0 ? (I)dn_of(seg[K - d + 1]) : (I)-1;
+      seg[K + d] = seg[K + d - 1] >= 0 ? (I)up_of(seg[K + d - 1]) : (I)-1;
     }
   }
   // no prefetch (batched levels: the walk is shared by the batch's vectors already)
   struct Pre {};
   __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
+  template <int K, class I>
+  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, I* seg) const {
     segment<K>(o, j, seg);
   }
 };
@@ -128,14 +132,14 @@ struct AxInner : AxTab {
   int64_t n;
   struct Pre {};
   __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
+  template <int K, class I>
+  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, I* seg) const {
     j = __ldg(jv + o);
-    seg[K] = o;
+    seg[K] = (I)o;
 #pragma unroll
     for (int d = 1; d <= K; ++d) {
-      seg[K - d] = j >= d ? o - d : -1;
-      seg[K + d] = (o + d < n && __ldg(jv + o + d) == j + d) ? o + d : -1;
+      seg[K - d] = j >= d ? (I)(o - d) : (I)-1;
+      seg[K + d] = (o + d < n && __ldg(jv + o + d) == j + d) ? (I)(o + d) : (I)-1;
     }
   }
 };
@@ -154,10 +158,10 @@ struct AxWin : AxTab {
   int kwin;  // K of the stored table (>= the level's K)
   struct Pre {};
   __device__ __forceinline__ Pre pre(int64_t) const { return {}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, int64_t* seg) const {
+  template <int K, class I>
+  __device__ __forceinline__ void segment_pre(const Pre&, int64_t o, int& j, I* seg) const {
     j = __ldg(jv + o);
-    seg[K] = o;
+    seg[K] = (I)o;
 #pragma unroll
     for (int d = 1; d <= K; ++d) {
       seg[K - d] = __ldg(win + (int64_t)(kwin - d) * n + o);
@@ -180,18 +184,18 @@ struct AxTabPf : AxTab {
     int32_t dn, up;
   };
   __device__ __forceinline__ Pre pre(int64_t o) const { return {__ldg(jv + o), __ldg(down + o), __ldg(up + o)}; }
-  template <int K>
-  __device__ __forceinline__ void segment_pre(const Pre& p, int64_t o, int& j, int64_t* seg) const {
+  template <int K, class I>
+  __device__ __forceinline__ void segment_pre(const Pre& p, int64_t o, int& j, I* seg) const {
     j = p.j;
-    seg[K] = o;
+    seg[K] = (I)o;
     if (K > 0) {
       seg[K - 1] = p.dn;
       seg[K + 1] = p.up;
     }
 #pragma unroll
     for (int d = 2; d <= K; ++d) {
-      seg[K - d] = seg[K - d + 1] >= 0 ? dn_of(seg[K - d + 1]) : -1;
-      seg[K + d] = seg[K + d - 1] >= 0 ? up_of(seg[K + d - 1]) : -1;
+      seg[K - d] = seg[K - d + 1] >= 0 ? (I)dn_of(seg[K - d + 1]) : (I)-1;
+      seg[K + d] = seg[K + d - 1] >= 0 ? (I)up_of(seg[K + d - 1]) : (I)-1;
     }
   }
 };
@@ -228,6 +232,10 @@ __device__ __forceinline__ void cdot_acc(double2 a, double2 b, double2& acc) {
 
 
 // ---------------------------------------------------------------- level kernel (hp_level.cu)
+
+// a present window ordinal as an unsigned element index
+__device__ __forceinline__ uint32_t lv_uidx(int32_t i) { return (uint32_t)i; }
+__device__ __forceinline__ int64_t lv_uidx(int64_t i) { return i; }
 
 constexpr int LV_MAXIN = 64;
 constexpr int LV_MAXTG = 16;  // targets accumulate in registers
@@ -270,8 +278,8 @@ struct LvLevel {
   __device__ __forceinline__ int ntg_() const { return ntg; }
   __device__ __forceinline__ int tg_buf_(int q) const { return tg_buf[q]; }
   // every input vector of the level: T_k x at o from the band rows, then its entries
-  template <int K, int TGN>
-  __device__ __forceinline__ void inputs(const double (&R)[K + 1][2 * K + 1], const int64_t (&seg)[2 * K + 1],
+  template <int K, int TGN, class I>
+  __device__ __forceinline__ void inputs(const double (&R)[K + 1][2 * K + 1], const I (&seg)[2 * K + 1],
                                          const double2* __restrict__ v, double2* __restrict__ slots, int64_t nbn,
                                          int64_t bo, int64_t o, double2 (&accs)[TGN]) const {
     constexpr int S = 2 * K + 1;
@@ -283,7 +291,7 @@ struct LvLevel {
       double2 xw[S];
 #pragma unroll
       for (int p = 0; p < S; ++p) {
-        xw[p] = ((need >> p) & 1u) && seg[p] >= 0 ? __ldg(x + seg[p]) : make_double2(0.0, 0.0);
+        xw[p] = ((need >> p) & 1u) && seg[p] >= 0 ? __ldg(x + lv_uidx(seg[p])) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int k = 0; k <= K; ++k) {
@@ -338,7 +346,7 @@ __device__ __forceinline__ double2 lv_band(const double (&R)[K + 1][2 * K + 1], 
   {                            \
     const double2* x_ = (ptr); \
     double2 xw_[2 * K + 1];
-#define LV_GEN_LOAD(p) xw_[p] = seg[p] >= 0 ? __ldg(x_ + seg[p]) : make_double2(0.0, 0.0);
+#define LV_GEN_LOAD(p) xw_[p] = seg[p] >= 0 ? __ldg(x_ + lv_uidx(seg[p])) : make_double2(0.0, 0.0);
 #define LV_GEN_T(k) \
   {                 \
     const double2 t_ = lv_band<K, k>(R, xw_);
@@ -383,7 +391,7 @@ __device__ __forceinline__ void lv_body(int64_t n, int64_t batch, const AX& ax, 
       pre_next = ax.pre(o_next);
     }
     // the axis line through o: seg[K + d] = ordinal of j + d e_a, or -1
-    int64_t seg[S];
+    typename AX::Idx seg[S];  // int32 on tabled sets
     int jo;
     ax.template segment_pre<K>(pre_o, o, jo, seg);
     // links of the window: lk[p] = sqrt(j_p / 2) couples positions p - 1 and p (cd at p = cu at

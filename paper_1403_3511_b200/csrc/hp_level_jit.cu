@@ -14,6 +14,7 @@
 #include <nvrtc.h>
 #include <cuda.h>
 
+#include <cctype>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -146,8 +147,8 @@ std::string kernel_source(const LvLevel& lv, const char* ax, const char* axs, in
   s += "\nnamespace hp {\nstruct LvGen {\n  double w[" + std::to_string(nw > 0 ? nw : 1) + "];\n";
   s += "  __device__ __forceinline__ int ntg_() const { return " + std::to_string(lv.ntg) + "; }\n";
   s += "  __device__ __forceinline__ int tg_buf_(int q) const { return " + tg + "; }\n";
-  s += "  template <int K, int TGN>\n"
-       "  __device__ __forceinline__ void inputs(const double (&R)[K + 1][2 * K + 1], const int64_t (&seg)[2 * K + 1],\n"
+  s += "  template <int K, int TGN, class I>\n"
+       "  __device__ __forceinline__ void inputs(const double (&R)[K + 1][2 * K + 1], const I (&seg)[2 * K + 1],\n"
        "                                         const double2* __restrict__ v, double2* __restrict__ slots,\n"
        "                                         int64_t nbn, int64_t bo, int64_t o, double2 (&accs)[TGN]) const {\n";
   s += body;
@@ -162,31 +163,60 @@ std::string kernel_source(const LvLevel& lv, const char* ax, const char* axs, in
   return s;
 }
 
-CUfunction compile_kernel(const std::string& src) {
+// spilled bytes ptxas reports for the kernel (--ptxas-options=-v lines in the NVRTC log)
+int spill_bytes(const std::string& log) {
+  int total = 0;
+  for (const char* tag : {"bytes spill stores", "bytes spill loads"}) {
+    const size_t p = log.find(tag);
+    if (p == std::string::npos) continue;
+    size_t q = p;
+    while (q > 0 && (log[q - 1] == ' ' || isdigit((unsigned char)log[q - 1]))) --q;
+    total += atoi(log.c_str() + q);
+  }
+  return total;
+}
+
+CUfunction compile_with(const std::string& src, int minb, int* spills) {
   const Rtc& r = rtc();
   nvrtcProgram prog = nullptr;
   if (r.create(&prog, src.c_str(), "hp_level_gen.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return nullptr;
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "-DHP_RTC=1"};
-  const nvrtcResult rc = r.compile(prog, 4, opts);
-  if (rc != NVRTC_SUCCESS || debug_on()) {
-    size_t ls = 0;
-    r.log_size(prog, &ls);
-    std::string log(ls, '\0');
-    if (ls > 1) r.log(prog, &log[0]);
-    if (rc != NVRTC_SUCCESS) fprintf(stderr, "[hp_level_jit] compilation failed:\n%s\n", log.c_str());
-  }
+  const std::string bounds = "-DLV_MINB=" + std::to_string(minb);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--ptxas-options=-v", bounds.c_str()};
+  const nvrtcResult rc = r.compile(prog, 5, opts);
+  size_t ls = 0;
+  r.log_size(prog, &ls);
+  std::string log(ls, '\0');
+  if (ls > 1) r.log(prog, &log[0]);
+  if (rc != NVRTC_SUCCESS) fprintf(stderr, "[hp_level_jit] compilation failed:\n%s\n", log.c_str());
+  *spills = spill_bytes(log);
   CUfunction fn = nullptr;
   if (rc == NVRTC_SUCCESS) {
     size_t cs = 0;
     if (r.cubin_size(prog, &cs) == NVRTC_SUCCESS && cs > 0) {
       std::vector<char> cubin(cs);
-      CUmodule mod = nullptr;  // kept loaded for the life of the process (cached below)
+      CUmodule mod = nullptr;  // kept loaded for the life of the process (cached by the caller)
       if (r.cubin(prog, cubin.data()) == NVRTC_SUCCESS && r.module_load(&mod, cubin.data()) == CUDA_SUCCESS &&
           r.module_get(&fn, mod, "k_level_gen") != CUDA_SUCCESS)
         fn = nullptr;
     }
   }
   r.destroy(&prog);
+  return fn;
+}
+
+// Resident blocks per SM: 4 (64 registers) unless that spills; a level whose window, band rows and
+// accumulators do not fit 64 registers runs faster spill-free at 2 blocks (128 registers) than
+// with more warps and local-memory traffic (cfg5, K = 3 levels: 444 ms at 4 blocks, 447 at 3, 406
+// at 2; the spill-free K = 2 levels of cfg3: 3.68 ms at 4 blocks, 4.55 at 3, 4.91 at 2).
+CUfunction compile_kernel(const std::string& src) {
+  int spills = 0;
+  if (const char* e = getenv("HP_LEVEL_JIT_MINB")) return compile_with(src, atoi(e), &spills);  // experiments
+  CUfunction fn = compile_with(src, 4, &spills);
+  if (fn && spills > 32) {
+    int spills2 = 0;
+    if (CUfunction fn2 = compile_with(src, 2, &spills2)) fn = fn2;
+    if (debug_on()) fprintf(stderr, "[hp_level_jit] %d spilled bytes at 4 blocks/SM -> 2 blocks/SM (%d)\n", spills, spills2);
+  }
   return fn;
 }
 
