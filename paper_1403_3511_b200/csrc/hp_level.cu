@@ -656,14 +656,14 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
   int64_t chunk = std::min<int64_t>(batch, (int64_t)(ws_bytes / per_vec));
   if (chunk < 1) return HP_OK;
   const int64_t n = s->n;
-  // blocks per SM of the grid-stride level kernels (HP_LEVEL_GRID overrides): batched levels 16
-  // (cfg5 659 -> 640 ms), single vectors 8 (cfg3: 4 5.79, 8 5.85, 16 5.92, 3 or 6 ~6.9 ms --
-  // wave quantisation against 4 resident blocks; profiles/r2/sweep_level.txt)
+  // blocks per SM of the grid-stride level kernels (HP_LEVEL_GRID overrides): batched levels 16,
+  // single vectors 4 = one resident wave (specialised kernels, profiles/r2/sweep_level.txt: cfg3
+  // 3.53 ms at 4, 3.68 at 8, 3.73 at 16; cfg5 418 / 412 / 406 / 398 ms at 4 / 8 / 16 / 32)
   static const int bps_env = [] {
     const char* e = getenv("HP_LEVEL_GRID");
     return e ? std::max(1, atoi(e)) : 0;
   }();
-  const int bps = bps_env ? bps_env : (batch > 1 ? 16 : 8);
+  const int bps = bps_env ? bps_env : (batch > 1 ? 16 : 4);
   const int grid = grid_for(n, 256, 148 * bps);
   const bool osc = flags & HP_ADD_OSC;
   // y must be written by the first level that targets it and osc/dot applied at the last
