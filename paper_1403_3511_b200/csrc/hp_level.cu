@@ -317,11 +317,26 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut,
   return P;
 }
 
-static void dump_plan(const LvProgram& P) {  // HP_LEVEL_DEBUG=1: planner output on stderr
+static void dump_plan(const LvProgram& P) {  // HP_LEVEL_DEBUG=1: planner output on stderr (2: every input)
+  const char* e = getenv("HP_LEVEL_DEBUG");
+  const bool detail = e && atoi(e) >= 2;
   fprintf(stderr, "[hp_level] %zu levels, %d slots, cost %.2f\n", P.levels.size(), P.nslots, P.cost);
   for (const LvLevel& L : P.levels) {
-    fprintf(stderr, "  axis %d K %d inputs %d targets %d accumulators*100+direct %d\n", L.axis, L.K, L.nin, L.ntg,
-            L.tgn * 100 + (int)L.d_start[L.nin]);
+    fprintf(stderr, "  axis %d K %d inputs %d targets %d (accumulators %d) direct children %d\n", L.axis, L.K, L.nin,
+            L.ntg, L.tgn, (int)L.d_start[L.nin]);
+    if (!detail) continue;
+    for (int q = 0; q < L.ntg; ++q) fprintf(stderr, "    target %d -> buffer %d\n", q, L.tg_buf[q]);
+    for (int i = 0; i < L.nin; ++i) {
+      fprintf(stderr, "    input buffer %d window %#x:", L.in_buf[i], L.in_pmask[i]);
+      for (int k = 0; k <= L.K; ++k) {
+        for (int q = 0; q < L.tgn; ++q)
+          if (((L.in_kmask[i] >> k) & 1) && L.wt[(i * (L.K + 1) + k) * L.tgn + q] != 0.0)
+            fprintf(stderr, " T%d->t%d", k, q);
+        for (int d = L.d_start[i]; d < L.d_start[i + 1]; ++d)
+          if (L.direct[d].k == k) fprintf(stderr, " T%d=>s%d", k, L.direct[d].slot);
+      }
+      fprintf(stderr, "\n");
+    }
   }
 }
 
