@@ -2,7 +2,11 @@
 //
 // Same operator and march as k_fg_single (hp_fg1.cuh):
 //   y = [c0 + sum_a P_a(X_a) + T_r0(X_0) G(X_1)] v  on a 4-D box (axes 0-based, axis 0 = j1),
-// one read of v and one write of y per coefficient.  What changes is the per-SM working set:
+// one read of v and one write of y per coefficient.  MIX selects the couplings: bit 0 the
+// (0,1) class above; bit 1 adds c02 T_1(X_0) T_1(X_2) (x1 x3: its axis-2 taps b +- 1 come from
+// A1 / the B2 boxes and join the same march-axis scatter); bit 3 adds c13 T_1(X_1) T_1(X_3)
+// (x2 x4: an in-plane term whose corner taps (a +- 1, c +- 1) lie inside box A1).  The other
+// pairs' corners are not staged.  What changes against k_fg_single is the per-SM working set:
 //
 // * Tiles are 8 x 8 x 16 (axes 1, 2, 3) = 1024 points instead of 512, so the halo staged per
 //   plane falls from 5x to 4x the tile (64 B/coef of TMA fills instead of 80): box A1 =
@@ -62,7 +66,8 @@ constexpr size_t Q_TOFF = Q_WOFF + (size_t)Q_MAXN * F1_WROW * sizeof(double);
 constexpr size_t Q_T2OFF = Q_TOFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
 constexpr size_t Q_T3OFF = Q_T2OFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
 constexpr int Q_T3N = Q_MAXN + 16;  // axis-3 table: [5][Q_T3N], transposed (16 lanes read 128 B)
-constexpr size_t Q_BOFF = Q_T3OFF + (size_t)5 * Q_T3N * sizeof(double);
+constexpr int Q_T3ROWS = 7;  // P3(-4, -2, 2, 4, 0) and B_{3,1}(-1, +1) (MIX & 8)
+constexpr size_t Q_BOFF = Q_T3OFF + (size_t)Q_T3ROWS * Q_T3N * sizeof(double);
 constexpr int Q_TC = 64;  // tile codes cached in shared memory
 constexpr size_t Q_SMEM = Q_BOFF + 2 * Q_S * sizeof(uint64_t) + (Q_S + Q_TC) * sizeof(int);
 
@@ -73,7 +78,7 @@ __device__ __forceinline__ void q_prefetch4(const CUtensorMap* m, int c0, int c1
                : "memory");
 }
 
-template <int NMIX, bool DOT>
+template <int MIX, bool DOT>
 __global__ void __launch_bounds__(Q_NT, 1)
     k_fg_quad(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB2,
               const double2* __restrict__ v, double2* __restrict__ y, const double* __restrict__ P,
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
   // {P0(p,0), P0(p+2,-2), P0(p-2,2), P0(p+4,-4), P0(p-4,4), B0(p+1,-1), B0(p-1,1), 0}
   for (int q = tid; q < n0; q += Q_NT) {
     auto p0 = [&](int r, int e) { return (r >= 0 && r < n0) ? P0[r * FG_W + e + FG_K] : 0.0; };
-    auto b0 = [&](int r, int e) { return (NMIX && r >= 0 && r < n0) ? B0[r * FG_W + e + FG_K] : 0.0; };
+    auto b0 = [&](int r, int e) { return (MIX && r >= 0 && r < n0) ? B0[r * FG_W + e + FG_K] : 0.0; };
     double* w = W + q * F1_WROW;
     w[0] = p0(q, 0);
     w[1] = p0(q + 2, -2);
@@ -125,10 +130,11 @@ __global__ void __launch_bounds__(Q_NT, 1)
     w[1] = ok ? P1[r * FG_W + FG_K - 2] : 0.0;
     w[2] = ok ? P1[r * FG_W + FG_K + 2] : 0.0;
     w[3] = ok ? P1[r * FG_W + FG_K + 4] : 0.0;
-    w[4] = ok && NMIX ? G[r * FG_W + FG_K - 1] : 0.0;
-    w[5] = ok && NMIX ? G[r * FG_W + FG_K + 1] : 0.0;
+    w[4] = ok && (MIX & 1) ? G[r * FG_W + FG_K - 1] : 0.0;
+    w[5] = ok && (MIX & 1) ? G[r * FG_W + FG_K + 1] : 0.0;
     w[6] = ok ? P1[r * FG_W + FG_K] : 0.0;
-    w[7] = 0.0;
+    // c13 B_{1,1}(r, -1): the band is symmetric, so B_{1,1}(r, +1) is the entry of row r + 1
+    w[7] = ok && (MIX & 8) ? G[(size_t)3 * FG_MAXN * FG_W + r * FG_W + FG_K - 1] : 0.0;
   }
   // axis-2 rows: {P2(r,-4), P2(r,-2), P2(r,2), P2(r,4), P2(r,0), 0, 0, 0}
   for (int r = tid; r < n2 + 8; r += Q_NT) {
@@ -139,7 +145,9 @@ __global__ void __launch_bounds__(Q_NT, 1)
     w[2] = ok ? P2[r * FG_W + FG_K + 2] : 0.0;
     w[3] = ok ? P2[r * FG_W + FG_K + 4] : 0.0;
     w[4] = ok ? P2[r * FG_W + FG_K] : 0.0;
-    w[5] = w[6] = w[7] = 0.0;
+    w[5] = ok && (MIX & 2) ? G[(size_t)2 * FG_MAXN * FG_W + r * FG_W + FG_K - 1] : 0.0;  // c02 B_{2,1}(r, -1)
+    w[6] = ok && (MIX & 2) ? G[(size_t)2 * FG_MAXN * FG_W + r * FG_W + FG_K + 1] : 0.0;  // c02 B_{2,1}(r, +1)
+    w[7] = 0.0;
   }
   // axis-3 columns, transposed: T3w[i][r] = P3(r, -4, -2, 2, 4, 0 for i = 0..4)
   for (int r = tid; r < Q_T3N; r += Q_NT) {
@@ -149,6 +157,10 @@ __global__ void __launch_bounds__(Q_NT, 1)
     T3w[2 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K + 2] : 0.0;
     T3w[3 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K + 4] : 0.0;
     T3w[4 * Q_T3N + r] = ok ? P3[r * FG_W + FG_K] : 0.0;
+    if (MIX & 8) {
+      T3w[5 * Q_T3N + r] = ok ? G[(size_t)4 * FG_MAXN * FG_W + r * FG_W + FG_K - 1] : 0.0;  // B_{3,1}(r, -1)
+      T3w[6 * Q_T3N + r] = ok ? G[(size_t)4 * FG_MAXN * FG_W + r * FG_W + FG_K + 1] : 0.0;  // B_{3,1}(r, +1)
+    }
   }
   __syncthreads();
 
@@ -321,24 +333,60 @@ __global__ void __launch_bounds__(Q_NT, 1)
             fma2(wb23.y, t3, rb);
             Q_FENCE();
           }
-          // phase C: coupling g = G(X_1) v at rows a, a+2, scattered through T_r0(X_0) to y(p +- 1)
-          if (NMIX) {
+          // phase C: couplings through the march axis, g = [G(X_1) + c02 T_1(X_2)] v at rows a, a+2,
+          // scattered through T_r0(X_0) to y(p +- 1)
+          if (MIX & 3) {
             const double2 ga = make_double2(QT1A(4), QT1A(5)), gb = make_double2(QT1B(4), QT1B(5));
             const double2 wcd = make_double2(wc.y, wd);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int o = oc + h * 2 * Q_RW;
-              const double2 m1 = st[o - Q_R1], p1 = st[o + Q_R1], p3 = st[o + 3 * Q_R1];
               double2* Ra = R[2 * h];
               double2* Rb = R[2 * h + 1];
-              double2 g = make_double2(ga.x * m1.x, ga.x * m1.y);
-              fma2(ga.y, p1, g);
+              double2 g = make_double2(0.0, 0.0), g2 = make_double2(0.0, 0.0);
+              if (MIX & 1) {
+                const double2 m1 = st[o - Q_R1], p1 = st[o + Q_R1], p3 = st[o + 3 * Q_R1];
+                g = make_double2(ga.x * m1.x, ga.x * m1.y);
+                fma2(ga.y, p1, g);
+                g2 = make_double2(gb.x * p1.x, gb.x * p1.y);
+                fma2(gb.y, p3, g2);
+              }
+              if (MIX & 2) {
+                // axis-2 taps t = (b + 2h) -+ 1 of rows a and a + 2 (A1 inside the tile, B2 boxes outside)
+                const int tm = b + 2 * h - 1, tp = b + 2 * h + 1;
+                const int om = o2(a, tm), op = o2(a, tp);
+                const int dm = (tm < 0 || tm >= Q_T2) ? 2 * Q_B2R1 : 2 * Q_R1, dp = (tp < 0 || tp >= Q_T2) ? 2 * Q_B2R1 : 2 * Q_R1;
+                const double cm = h ? QT2B(5) : QT2A(5), cp = h ? QT2B(6) : QT2A(6);
+                fma2(cm, st[om], g);
+                fma2(cp, st[op], g);
+                fma2(cm, st[om + dm], g2);
+                fma2(cp, st[op + dp], g2);
+              }
               fma2(wcd.x, g, Ra[(U + 1) & 7]);
               fma2(wcd.y, g, Ra[(U + 7) & 7]);
-              g = make_double2(gb.x * p1.x, gb.x * p1.y);
-              fma2(gb.y, p3, g);
-              fma2(wcd.x, g, Rb[(U + 1) & 7]);
-              fma2(wcd.y, g, Rb[(U + 7) & 7]);
+              fma2(wcd.x, g2, Rb[(U + 1) & 7]);
+              fma2(wcd.y, g2, Rb[(U + 7) & 7]);
+            }
+            Q_FENCE();
+          }
+          // in-plane coupling c13 T_1(X_1) T_1(X_3) v: corner taps (a +- 1, c +- 1) and (a + 1 | a + 3, c +- 1)
+          if (MIX & 8) {
+            const double w3m = Q3(5), w3p = Q3(6);
+            const double s0 = QT1A(7), s1 = T1w[(J1 + 1) * Q_T1W + 7], s2 = QT1B(7), s3 = T1w[(J1 + 3) * Q_T1W + 7];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int o = oc + h * 2 * Q_RW;
+              double2 hm = make_double2(0.0, 0.0), h1 = hm, h3 = hm;
+              fma2(w3m, st[o - Q_R1 - 1], hm);
+              fma2(w3p, st[o - Q_R1 + 1], hm);
+              fma2(w3m, st[o + Q_R1 - 1], h1);
+              fma2(w3p, st[o + Q_R1 + 1], h1);
+              fma2(w3m, st[o + 3 * Q_R1 - 1], h3);
+              fma2(w3p, st[o + 3 * Q_R1 + 1], h3);
+              fma2(s0, hm, R[2 * h][U]);
+              fma2(s1, h1, R[2 * h][U]);
+              fma2(s2, h1, R[2 * h + 1][U]);
+              fma2(s3, h3, R[2 * h + 1][U]);
             }
             Q_FENCE();
           }

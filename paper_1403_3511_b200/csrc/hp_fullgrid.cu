@@ -109,6 +109,10 @@ struct FgPlan {
   unsigned mask[4] = {0, 0, 0, 0}; // nonzero diagonals of the combined single-axis bands
   unsigned maskG = 0;              // nonzero diagonals of the mixed-term axis-2 bands G_m
   bool twopass = true;             // the cube fits the two-pass kernels' chunking (single pass: any side)
+  // further T_1 (x) T_1 couplings of the single-pass quad kernel: axes (0,2) and (1,3), i.e.
+  // x1 x3 and x2 x4 (the halo boxes of k_fg_quad hold their taps; (1,2) and (2,3) corners are not staged)
+  double cx02 = 0.0, cx13 = 0.0;
+  bool extra() const { return cx02 != 0.0 || cx13 != 0.0; }
 };
 
 static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch, int flags) {
@@ -137,6 +141,14 @@ static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dt
       P.wm[m][t.r[1]] += t.alpha;
       continue;
     }
+    if (na == 2 && t.r[act[0]] == 1 && t.r[act[1]] == 1 && act[0] == 0 && act[1] == 2) {
+      P.cx02 += t.alpha;
+      continue;
+    }
+    if (na == 2 && t.r[act[0]] == 1 && t.r[act[1]] == 1 && act[0] == 1 && act[1] == 3) {
+      P.cx13 += t.alpha;
+      continue;
+    }
     return P;
   }
   for (int m = 0; m < P.nmix; ++m) P.rm = std::max(P.rm, P.r0[m]);
@@ -161,9 +173,13 @@ static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dt
 
 // ---------------------------------------------------------------- kernels
 
+// band tables in the workspace: P[4] | G[2] (mixed classes of axes (0,1)) | cx02 B_{2,1} | cx13 B_{1,1} | B_{3,1}
+constexpr int FG_NTAB = 9;
+
 struct CombineArgs {
   double ws[4][FG_K + 1];
   double wm[2][FG_K + 1];
+  double cx02, cx13;
   int side[4];
   int joff0;
   int nmix;
@@ -177,7 +193,7 @@ struct CombineArgs {
 __global__ void k_fg_combine(const double* __restrict__ basis, double* __restrict__ P, double* __restrict__ G,
                              CombineArgs A) {
   const size_t bs = (size_t)(FG_K + 1) * FG_MAXN * FG_W;
-  int total = (4 + 2) * FG_MAXN * FG_W;
+  int total = FG_NTAB * FG_MAXN * FG_W;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     int tab = idx / (FG_MAXN * FG_W);
     int rem = idx % (FG_MAXN * FG_W);
@@ -202,7 +218,7 @@ __global__ void k_fg_combine(const double* __restrict__ basis, double* __restric
         }
       }
       P[(size_t)a * FG_MAXN * FG_W + rem] = acc;
-    } else {
+    } else if (tab < 6) {
       int m = tab - 4;
       int n = A.side[1];
       double acc = 0.0;
@@ -210,6 +226,12 @@ __global__ void k_fg_combine(const double* __restrict__ basis, double* __restric
         for (int k = 0; k <= FG_K; ++k)
           if (A.wm[m][k] != 0.0) acc += A.wm[m][k] * basis[1 * bs + ((size_t)k * n + j) * FG_W + d];
       G[(size_t)m * FG_MAXN * FG_W + rem] = acc;
+    } else {
+      // T_1 bands of the further couplings: cx02 B_{2,1}, cx13 B_{1,1}, B_{3,1}
+      const int a = tab == 6 ? 2 : (tab == 7 ? 1 : 3);
+      const double c = tab == 6 ? A.cx02 : (tab == 7 ? A.cx13 : 1.0);
+      const int n = A.side[a];
+      G[(size_t)(tab - 4) * FG_MAXN * FG_W + rem] = (j < n && c != 0.0) ? c * basis[a * bs + ((size_t)1 * n + j) * FG_W + d] : 0.0;
     }
   }
 }
@@ -326,6 +348,8 @@ static int sm_count() {
 }
 
 // k_fg_quad: 8 x 8 x 16 tiles, sides <= Q_MAXN
+// MIX: bit 0 = the (0,1) coupling class, bit 1 = (0,2), bit 3 = (1,3) (hp_fg4.cuh)
+constexpr int FG_MIX_ALL = 1 | 2 | 8;
 template <int NMIX>
 static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, const double* P, const double* G,
                              const FgPlan& F, cudaStream_t st, DotOut* dot, bool* launched, int plo, int phi) {
@@ -335,7 +359,8 @@ static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, co
   hp_status rc = make_tiles(s, Q_T1, Q_T2, Q_T3, &s->fg_tiles4, &s->fg_ntiles4);
   if (rc) return rc;
   const int n0 = s->side[0];
-  const double* B0 = s->fg_basis + (size_t)(NMIX ? F.r0[0] : 0) * n0 * FG_W;  // axis 0, degree r0
+  // axis 0 band that carries the march-axis couplings: degree r0 of the (0,1) class, T_1 otherwise
+  const double* B0 = s->fg_basis + (size_t)(NMIX ? (F.nmix ? F.r0[0] : 1) : 0) * n0 * FG_W;
   const int grid = std::min(s->fg_ntiles4, sm_count());
   const bool use_dot = dot && dot->partial && grid <= dot->capacity;
   double2* dotp = use_dot ? dot->partial : nullptr;
@@ -362,6 +387,7 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
   *launched = false;
   if (fg_quad() && s->side[0] <= Q_MAXN && s->side[1] <= Q_MAXN)
     return launch_quad<NMIX>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+  if constexpr (NMIX > 1) return HP_OK;  // the further couplings exist in k_fg_quad only
   CUtensorMap mA1, mB2;
   if (!tma_map(&mA1, v, s->side, 2 * F1_RW, F1_T2, F1_T1 + 2 * F1_H) ||
       !tma_map(&mB2, v, s->side, 2 * F1_T3, F1_H, F1_T1))
@@ -373,8 +399,9 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
   const int grid = std::min(s->fg_ntiles, sm_count());
   const bool use_dot = dot && dot->partial && grid <= dot->capacity;
   const int np = fg_np();
-  auto kern = np == 1 ? (use_dot ? k_fg_single<NMIX, true, 1> : k_fg_single<NMIX, false, 1>)
-                      : (use_dot ? k_fg_single<NMIX, true, 2> : k_fg_single<NMIX, false, 2>);
+  constexpr int NM1 = NMIX & 1;
+  auto kern = np == 1 ? (use_dot ? k_fg_single<NM1, true, 1> : k_fg_single<NM1, false, 1>)
+                      : (use_dot ? k_fg_single<NM1, true, 2> : k_fg_single<NM1, false, 2>);
   HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F1_SMEM));
   kern<<<grid, F1_POINTS / np, F1_SMEM, st>>>(mA1, mB2, v, y, P, G, B0, s->fg_tiles, s->fg_ntiles, n0, s->side[1],
                                               s->side[2], s->side[3], use_dot ? dot->partial : nullptr, fg_exp(),
@@ -383,6 +410,23 @@ static hp_status launch_single(const hp_set_s* s, const double2* v, double2* y, 
   if (use_dot) dot->n = grid;
   *launched = true;
   return HP_OK;
+}
+
+static hp_status launch_single_for(const FgPlan& F, const hp_set_s* s, const double2* v, double2* y, const double* P,
+                                   const double* G, cudaStream_t st, DotOut* dot, bool* launched, int plo = 0,
+                                   int phi = -1) {
+  // one instantiation per set of couplings present (an absent coupling costs no shared-memory taps)
+  const int mix = (F.nmix ? 1 : 0) | (F.cx02 != 0.0 ? 2 : 0) | (F.cx13 != 0.0 ? 8 : 0);
+  switch (mix) {
+    case 0: return launch_single<0>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+    case 1: return launch_single<1>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+    case 2: return launch_single<2>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+    case 3: return launch_single<3>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+    case 8: return launch_single<8>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+    case 9: return launch_single<9>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+    case 10: return launch_single<10>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+    default: return launch_single<FG_MIX_ALL>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+  }
 }
 
 template <unsigned M2, unsigned M3>
@@ -443,7 +487,7 @@ size_t fullgrid_workspace_bytes(const hp_set_s* s, const std::vector<Term>& term
   FgPlan F = classify(s, terms, dtype, batch, flags);
   if (!F.ok) return 0;
   // bands | u (two-pass kernels) | per-CTA dot partials of the plane-range entry point
-  return (size_t)(4 + 2) * FG_MAXN * FG_W * sizeof(double) + 256 + (size_t)s->n * sizeof(double2) + FG_DOTP_BYTES;
+  return (size_t)FG_NTAB * FG_MAXN * FG_W * sizeof(double) + 256 + (size_t)s->n * sizeof(double2) + FG_DOTP_BYTES;
 }
 
 // classification + band tables; *ok = false when the fused evaluator does not cover the call
@@ -471,6 +515,8 @@ static hp_status fg_prepare(const hp_set_s* s, const std::vector<Term>& terms, d
     for (int k = 0; k <= FG_K; ++k) A.wm[m][k] = F.wm[m][k];
   A.joff0 = s->lo;
   A.nmix = F.nmix;
+  A.cx02 = F.cx02;
+  A.cx13 = F.cx13;
   A.c0 = F.c0;
   A.osc = (flags & HP_ADD_OSC) ? 1 : 0;
   A.sq = sq;
@@ -487,6 +533,10 @@ static bool fg_single_class(const FgPlan& F) {
   return fg_single_enabled() && even &&
          (F.nmix == 0 || (F.nmix == 1 && F.rm == 1 && (F.maskG & ~FG_MASK_PM1) == 0));
 }
+// the (0,2) / (1,3) couplings exist in k_fg_quad only (sides <= Q_MAXN)
+static bool fg_extra_ok(const hp_set_s* s, const FgPlan& F) {
+  return !F.extra() || (fg_quad() && s->side[0] <= Q_MAXN && s->side[1] <= Q_MAXN && fg_single_class(F));
+}
 
 hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                          const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
@@ -499,17 +549,16 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   if (rc || !ok) return rc;
   double* P = (double*)ws;
   double* G = P + 4 * FG_MAXN * FG_W;
-  double2* u = (double2*)((char*)ws + (((size_t)6 * FG_MAXN * FG_W * sizeof(double) + 255) & ~(size_t)255));
+  double2* u = (double2*)((char*)ws + (((size_t)FG_NTAB * FG_MAXN * FG_W * sizeof(double) + 255) & ~(size_t)255));
   const double2* v = (const double2*)in;
   double2* y = (double2*)out;
   const bool even = F.mask[0] == FG_MASK_EVEN && F.mask[2] == FG_MASK_EVEN && F.mask[3] == FG_MASK_EVEN;
   // single pass for the even-band class (cfg4); a batch runs one launch per vector
-  if (fg_single_class(F)) {
+  if (fg_single_class(F) && fg_extra_ok(s, F)) {
     bool launched = false;
     for (int64_t b = 0; b < batch; ++b) {
       const int64_t off = b * s->n;
-      rc = F.nmix ? launch_single<1>(s, v + off, y + off, P, G, F, st, batch == 1 ? dot : nullptr, &launched)
-                  : launch_single<0>(s, v + off, y + off, P, G, F, st, batch == 1 ? dot : nullptr, &launched);
+      rc = launch_single_for(F, s, v + off, y + off, P, G, st, batch == 1 ? dot : nullptr, &launched);
       if (rc) return rc;
       if (!launched) break;
     }
@@ -519,7 +568,7 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
     }
   }
   // the two-pass kernels take one vector and need their chunking: otherwise the level evaluator
-  if (batch != 1 || !F.twopass) return HP_OK;
+  if (batch != 1 || !F.twopass || F.extra()) return HP_OK;
   // pass B
   rc = even ? launch_inner<FG_MASK_EVEN, FG_MASK_EVEN>(s, v, u, P, st)
             : launch_inner<FG_MASK_ALL, FG_MASK_ALL>(s, v, u, P, st);
@@ -576,7 +625,7 @@ hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& term
                                 cudaStream_t st, bool* done, double* dot_accum, double sq) {
   *done = false;
   FgPlan F = classify(s, terms, dtype, 1, flags);
-  if (!F.ok || !fg_single_class(F)) return HP_OK;
+  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F)) return HP_OK;
   if (plo == phi) {  // support query: nothing to compute
     *done = ws_bytes >= fullgrid_workspace_bytes(s, terms, dtype, 1, flags);
     return HP_OK;
@@ -593,8 +642,7 @@ hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& term
     d.capacity = FG_DOTP;
   }
   DotOut* dp = dot_accum ? &d : nullptr;
-  rc = F.nmix ? launch_single<1>(s, (const double2*)in, (double2*)out, P, G, F, st, dp, &launched, plo, phi)
-              : launch_single<0>(s, (const double2*)in, (double2*)out, P, G, F, st, dp, &launched, plo, phi);
+  rc = launch_single_for(F, s, (const double2*)in, (double2*)out, P, G, st, dp, &launched, plo, phi);
   if (rc) return rc;
   if (launched && dot_accum) {
     if (d.n == 0) return fail(HP_ERR_RUNTIME, "plane-range matvec: fused dot unavailable");
@@ -638,7 +686,7 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
                                   void* ws, size_t ws_bytes, cudaStream_t st, bool* done) {
   *done = false;
   FgPlan F = classify(s, terms, dtype, 1, flags);
-  if (!F.ok || !fg_single_class(F)) return HP_OK;
+  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F)) return HP_OK;
   bool ok = false;
   hp_status rc = fg_prepare(s, terms, halfwidth, dtype, 1, flags, ws, ws_bytes, st, &F, &ok);
   if (rc || !ok) return rc;
@@ -671,10 +719,7 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
     const int p0 = k * C, p1 = std::min(n0, p0 + C);
     HP_CUDA(cudaStreamWaitEvent(st, ev[std::min(k + ahead, nch - 1)], 0));
     bool launched = false;
-    rc = F.nmix ? launch_single<1>(s, (const double2*)in_dev, (double2*)out_dev, P, G, F, st, nullptr, &launched,
-                                   p0, p1)
-                : launch_single<0>(s, (const double2*)in_dev, (double2*)out_dev, P, G, F, st, nullptr, &launched,
-                                   p0, p1);
+    rc = launch_single_for(F, s, (const double2*)in_dev, (double2*)out_dev, P, G, st, nullptr, &launched, p0, p1);
     if (rc) return rc;
     if (!launched) return fail(HP_ERR_RUNTIME, "streamed matvec: TMA descriptors unavailable");
     HP_CUDA(cudaEventRecord(ev[nch + k], st));

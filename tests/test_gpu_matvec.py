@@ -336,6 +336,53 @@ def test_fused_fullgrid_sizes_and_slabs(hp, bound):
         assert rel_l2(hp.get_applier(sl).apply_hamiltonian(ap, x), ob.hamiltonian(ap.degrees, ap.coeffs, 16.0, x)) < TOL
 
 
+def _coupled_potential(c01, c02, c13):
+    """cfg4's potential with further pair couplings: x1 x2 (c01), x1 x3 (c02), x2 x4 (c13)."""
+    def w(p, t):
+        return (0.5 * (p * p).sum(axis=-1) + c01 * math.cos(2.0 * t) * p[:, 0] * p[:, 1] + c02 * p[:, 0] * p[:, 2]
+                + c13 * p[:, 1] * p[:, 3] + 0.01 * (p ** 4).sum(axis=-1))
+    return w
+
+
+@pytest.mark.parametrize("cpl", [(0.0, 0.07, 0.0), (0.0, 0.0, 0.05), (0.1, 0.07, 0.05)], ids=["x1x3", "x2x4", "all"])
+@pytest.mark.parametrize("bound", [5, 11, 20])
+def test_fused_fullgrid_further_couplings(hp, rng, bound, cpl):
+    """The single-pass quad kernel's wider class (k_fg_quad<MIX>: x1 x3 through the march-axis
+    scatter, x2 x4 as an in-plane corner term) against the oracle: ragged cubes, j1-slabs, a
+    batch, the oscillator, and the in-kernel rows of x^H A x."""
+    import torch
+
+    from paper_1403_3511_b200 import _native as nat
+    from paper_1403_3511_b200.potential_approx import custom_potential, interpolate
+
+    ap = interpolate(custom_potential(_coupled_potential(*cpl), 4, 16.0), 4, 0.3)
+    side = bound + 1
+    s = hp.build_full(4, bound)
+    oa = O.applier_for_full(4, bound)
+    appl = hp.get_applier(s)
+    V = rng.standard_normal((2, s.size)) + 1j * rng.standard_normal((2, s.size))
+    Y = appl.apply_polynomial(ap, V)
+    for b in range(2):
+        assert rel_l2(Y[b], oa.polynomial(ap.degrees, ap.coeffs, 16.0, V[b])) < TOL
+    assert rel_l2(appl.apply_hamiltonian(ap, V[0]), oa.hamiltonian(ap.degrees, ap.coeffs, 16.0, V[0])) < TOL
+    plane = side ** 3
+    for lo, hi in [(0, side // 2), (side // 3, side), (1, max(2, side - 1))]:
+        sl = hp.build_slab(4, bound, lo, hi)
+        ob = O.applier_for_slab(4, bound, lo, hi)
+        x = np.ascontiguousarray(V[1][lo * plane:hi * plane])
+        assert rel_l2(hp.get_applier(sl).apply_hamiltonian(ap, x), ob.hamiltonian(ap.degrees, ap.coeffs, 16.0, x)) < TOL
+    # plane ranges with the fused dot (the evaluator the Lanczos loop uses)
+    x = torch.from_numpy(V[0]).cuda()
+    y = torch.empty_like(x)
+    dot = torch.zeros(2, dtype=torch.float64, device="cuda")
+    cuts = [0, side // 3, side // 3 + 1, side]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        assert appl.apply_planes_into(ap, x, y, lo, hi, nat.HP_ADD_OSC, dot=dot)
+    want = torch.vdot(x, y)
+    assert abs(complex(dot[0].item(), dot[1].item()) - complex(want)) <= 1e-13 * abs(complex(want))
+    assert rel_l2(y.cpu().numpy(), oa.hamiltonian(ap.degrees, ap.coeffs, 16.0, V[0])) < TOL
+
+
 @pytest.mark.slow
 def test_cfg4_full_size_slab_vs_oracle(hp):
     """Full-size cfg4 (2.7e8 coefficients): GPU output on planes j1 in [62, 64) equals the oracle
