@@ -33,13 +33,11 @@
 #ifndef Q_FENCES
 #define Q_FENCES 0  // compiler fences between load phases: off measured 0.8% faster (2.416 vs 2.434 ms)
 #endif
-#if Q_FENCES
-#define Q_FENCE() asm volatile("" ::: "memory")
-#else
-#define Q_FENCE() \
-  do {            \
+// (the instantiation with all three couplings keeps them: its live ranges spill otherwise)
+#define Q_FENCE()                                                   \
+  do {                                                              \
+    if (Q_FENCES || MIX == 11) asm volatile("" ::: "memory"); \
   } while (0)
-#endif
 
 namespace hp {
 
@@ -351,6 +349,7 @@ __global__ void __launch_bounds__(Q_NT, 1)
                 g2 = make_double2(gb.x * p1.x, gb.x * p1.y);
                 fma2(gb.y, p3, g2);
               }
+              if ((MIX & 3) == 3) Q_FENCE();
               if (MIX & 2) {
                 // axis-2 taps t = (b + 2h) -+ 1 of rows a and a + 2 (A1 inside the tile, B2 boxes outside)
                 const int tm = b + 2 * h - 1, tp = b + 2 * h + 1;

@@ -365,6 +365,13 @@ static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, co
   const bool use_dot = dot && dot->partial && grid <= dot->capacity;
   double2* dotp = use_dot ? dot->partial : nullptr;
   auto kern = use_dot ? k_fg_quad<NMIX, true> : k_fg_quad<NMIX, false>;
+  if (NMIX == FG_MIX_ALL && !use_dot && grid <= FG_DOTP) {
+    // all three couplings: ptxas spills the plain instantiation inside the march (152 bytes of
+    // reloads per step, 4.9 ms on the cfg4 cube) but not the one with the fused dot, so that one
+    // runs, its partials going to the workspace's dot region (behind the tables and the u vector)
+    kern = k_fg_quad<NMIX, true>;
+    dotp = (double2*)((char*)P + (size_t)FG_NTAB * FG_MAXN * FG_W * sizeof(double) + 256 + (size_t)s->n * sizeof(double2));
+  }
   HP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q_SMEM));
   // exp = 0: k_fg_quad keeps the experiment slot of k_fg_single's signature (dropping it moves
   // ptxas to a spilling allocation of the 255-register kernel)
