@@ -286,6 +286,7 @@ struct LvLevel {
     for (int ii = 0; ii < nin; ++ii) {
       const int ib = in_buf[ii];
       const double2* x = ib == -2 ? v + bo : slots + (int64_t)ib * nbn + bo;
+      asm volatile("" : "+l"(x));  // formed once per input, not rematerialised at every load
       const unsigned need = in_pmask[ii];  // window positions some entry of this input reads
       const unsigned km = in_kmask[ii], dm = in_dmask[ii];
       double2 xw[S];
@@ -342,9 +343,10 @@ __device__ __forceinline__ double2 lv_band(const double (&R)[K + 1][2 * K + 1], 
 // Pieces of a runtime-specialised level (hp_level_jit.cu writes LvGen::inputs() as a sequence of
 // these with literal arguments; `w` is the level's weight array, a kernel parameter):
 //   LV_GEN_IN(ptr) LV_GEN_LOAD(p).. { LV_GEN_T(k) LV_GEN_ACC(q, wi).. LV_GEN_DIRECT(slot, wi).. LV_GEN_T_END }.. LV_GEN_IN_END
-#define LV_GEN_IN(ptr)         \
-  {                            \
-    const double2* x_ = (ptr); \
+#define LV_GEN_IN(ptr)                                                                       \
+  {                                                                                          \
+    const double2* x_ = (ptr);                                                               \
+    asm volatile("" : "+l"(x_)); /* formed once per input, not rematerialised at every load */ \
     double2 xw_[2 * K + 1];
 #define LV_GEN_LOAD(p) xw_[p] = seg[p] >= 0 ? __ldg(x_ + lv_uidx(seg[p])) : make_double2(0.0, 0.0);
 #define LV_GEN_T(k) \

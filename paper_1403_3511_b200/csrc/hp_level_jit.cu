@@ -252,7 +252,15 @@ bool level_jit_launch(int device, const char* ax_name, const void* ax, const cha
     std::lock_guard<std::mutex> g(mtx);
     auto it = cache.find(key);
     if (it == cache.end()) {
-      fn = compile_kernel(kernel_source(lv, ax_name, axs_name, (int)w.size()));
+      const std::string src = kernel_source(lv, ax_name, axs_name, (int)w.size());
+      if (const char* dir = getenv("HP_LEVEL_JIT_DUMP")) {  // keep the generated sources (inspection with nvcc / cuobjdump)
+        const std::string path = std::string(dir) + "/hp_level_gen_" + std::to_string(cache.size()) + ".cu";
+        if (FILE* f = fopen(path.c_str(), "w")) {
+          fwrite(src.data(), 1, src.size(), f);
+          fclose(f);
+        }
+      }
+      fn = compile_kernel(src);
       if (debug_on())
         fprintf(stderr, "[hp_level_jit] axis %d K %d: %s (%zu weights)\n", lv.axis, lv.K, fn ? "compiled" : "FAILED",
                 w.size());
