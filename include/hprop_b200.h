@@ -62,6 +62,13 @@ const char* hp_last_error(void);
 int hp_device_count(void);
 /* number of kernels this library has launched in the process so far */
 int64_t hp_launch_count(void);
+/* Compiles (NVRTC, no device needed, nothing launched) the run-time specialised level kernels
+ * of the polynomial `degrees`/`coeffs` (as in hp_apply_polynomial) for both set kinds (tabled,
+ * boxed); *nkernels_out = kernels compiled.  HP_ERR_RUNTIME if NVRTC is unavailable or a
+ * compilation fails.  The build check of the path hp_apply_polynomial takes on large sets
+ * (fast_apply.py:110-164; csrc/hp_level_jit.cu). */
+hp_status hp_level_jit_selftest(int dim, const int32_t* degrees, const double* coeffs, int nterms,
+                                int* nkernels_out);
 
 /* ---- index sets (index_set.py) ------------------------------------------ */
 

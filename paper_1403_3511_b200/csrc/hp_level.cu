@@ -444,6 +444,8 @@ bool level_jit_launch(int device, const char* ax_name, const void* ax, const cha
                       double two_L, const double2* v, double2* slots, double2* y, int first, int osc, double2* dotp,
                       const int32_t* perm, const double* sqtab);
 
+bool level_jit_compile_only(const LvLevel& lv, const char* ax_name, const char* axs_name);
+
 // the specialised kernel of a large level if there is one, else the instantiation whose accumulator
 // count matches the level's dense weight table
 template <int K, class AX, class AXS>
@@ -722,3 +724,25 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
 }
 
 }  // namespace hp
+
+extern "C" hp_status hp_level_jit_selftest(int dim, const int32_t* degrees, const double* coeffs, int nterms,
+                                           int* nkernels_out) {
+  using namespace hp;
+  if (nkernels_out) *nkernels_out = 0;
+  if (dim < 1 || dim > HP_MAXDIM || nterms < 1 || !degrees || !coeffs)
+    return fail(HP_ERR_VALUE, "hp_level_jit_selftest: bad arguments");
+  const auto terms = make_terms(dim, degrees, coeffs, nterms);
+  const LvProgram P = plan_levels(dim, terms);
+  if (!P.ok) return fail(HP_ERR_VALUE, "hp_level_jit_selftest: the level planner does not cover this polynomial");
+  int n = 0;
+  for (const LvLevel& lv : P.levels) {
+    if (!level_jit_compile_only(lv, AxTab::name(), LvAllTab::name()) ||
+        !level_jit_compile_only(lv, AxBox::name(), LvAllBox::name()))
+      return fail(HP_ERR_RUNTIME, "hp_level_jit_selftest: NVRTC unavailable or compilation failed (axis " +
+                                      std::to_string(lv.axis) + ")");
+    n += 2;
+  }
+  if (nkernels_out) *nkernels_out = n;
+  return HP_OK;
+}
+

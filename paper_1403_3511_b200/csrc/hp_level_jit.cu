@@ -34,7 +34,8 @@ const char* const kDeviceSource =
     ;
 
 struct Rtc {
-  bool ok = false;
+  bool ok = false;        // NVRTC and the driver entry points
+  bool compiler = false;  // NVRTC alone (compilation without a device: hp_level_jit_selftest)
   decltype(&nvrtcCreateProgram) create = nullptr;
   decltype(&nvrtcCompileProgram) compile = nullptr;
   decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
@@ -72,6 +73,7 @@ Rtc load_rtc() {
   HP_SYM(cubin, "nvrtcGetCUBIN");
   HP_SYM(destroy, "nvrtcDestroyProgram");
 #undef HP_SYM
+  r.compiler = true;
   // driver entry points through the runtime (no link-time dependency on libcuda)
   cudaDriverEntryPointQueryResult q;
   void* f = nullptr;
@@ -176,10 +178,11 @@ int spill_bytes(const std::string& log) {
   return total;
 }
 
-CUfunction compile_with(const std::string& src, int minb, int* spills) {
+// NVRTC: source -> cubin (no device needed); *spills = bytes ptxas spilled
+bool compile_cubin(const std::string& src, int minb, int* spills, std::vector<char>* cubin) {
   const Rtc& r = rtc();
   nvrtcProgram prog = nullptr;
-  if (r.create(&prog, src.c_str(), "hp_level_gen.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return nullptr;
+  if (r.create(&prog, src.c_str(), "hp_level_gen.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return false;
   const std::string bounds = "-DLV_MINB=" + std::to_string(minb);
   const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--ptxas-options=-v", bounds.c_str()};
   const nvrtcResult rc = r.compile(prog, 5, opts);
@@ -189,18 +192,25 @@ CUfunction compile_with(const std::string& src, int minb, int* spills) {
   if (ls > 1) r.log(prog, &log[0]);
   if (rc != NVRTC_SUCCESS) fprintf(stderr, "[hp_level_jit] compilation failed:\n%s\n", log.c_str());
   *spills = spill_bytes(log);
-  CUfunction fn = nullptr;
-  if (rc == NVRTC_SUCCESS) {
-    size_t cs = 0;
-    if (r.cubin_size(prog, &cs) == NVRTC_SUCCESS && cs > 0) {
-      std::vector<char> cubin(cs);
-      CUmodule mod = nullptr;  // kept loaded for the life of the process (cached by the caller)
-      if (r.cubin(prog, cubin.data()) == NVRTC_SUCCESS && r.module_load(&mod, cubin.data()) == CUDA_SUCCESS &&
-          r.module_get(&fn, mod, "k_level_gen") != CUDA_SUCCESS)
-        fn = nullptr;
-    }
+  bool ok = false;
+  size_t cs = 0;
+  if (rc == NVRTC_SUCCESS && r.cubin_size(prog, &cs) == NVRTC_SUCCESS && cs > 0) {
+    cubin->resize(cs);
+    ok = r.cubin(prog, cubin->data()) == NVRTC_SUCCESS;
   }
   r.destroy(&prog);
+  return ok;
+}
+
+CUfunction compile_with(const std::string& src, int minb, int* spills) {
+  std::vector<char> cubin;
+  if (!compile_cubin(src, minb, spills, &cubin)) return nullptr;
+  const Rtc& r = rtc();
+  CUmodule mod = nullptr;  // kept loaded for the life of the process (cached by the caller)
+  CUfunction fn = nullptr;
+  if (!r.module_load || r.module_load(&mod, cubin.data()) != CUDA_SUCCESS ||
+      r.module_get(&fn, mod, "k_level_gen") != CUDA_SUCCESS)
+    return nullptr;
   return fn;
 }
 
@@ -221,6 +231,16 @@ CUfunction compile_kernel(const std::string& src) {
 }
 
 }  // namespace
+
+// compiles one level for the given axis views without loading it (no device needed)
+bool level_jit_compile_only(const LvLevel& lv, const char* ax_name, const char* axs_name) {
+  if (!rtc().compiler) return false;
+  std::vector<double> w;
+  walk_level(lv, nullptr, &w, nullptr);
+  int spills = 0;
+  std::vector<char> cubin;
+  return compile_cubin(kernel_source(lv, ax_name, axs_name, (int)w.size()), 4, &spills, &cubin);
+}
 
 bool level_jit_enabled(int64_t work) {
 #ifdef HP_DEVICE_CHECKS
@@ -251,6 +271,7 @@ bool level_jit_launch(int device, const char* ax_name, const void* ax, const cha
   {
     std::lock_guard<std::mutex> g(mtx);
     auto it = cache.find(key);
+    if (it == cache.end() && cache.size() >= 1024) return false;  // modules stay loaded: bounded
     if (it == cache.end()) {
       const std::string src = kernel_source(lv, ax_name, axs_name, (int)w.size());
       if (const char* dir = getenv("HP_LEVEL_JIT_DUMP")) {  // keep the generated sources (inspection with nvcc / cuobjdump)

@@ -47,3 +47,37 @@ def test_product_does_not_import_oracle():
         for line in f.read_text().splitlines():
             s = line.strip()
             assert not (s.startswith("import oracle") or s.startswith("from oracle")), f
+
+
+def test_runtime_specialised_level_kernels_compile():
+    """The level kernels hp_apply_polynomial compiles at run time for large sets (NVRTC,
+    csrc/hp_level_jit.cu) build for sm_100a here, without a device: cfg3's polynomial and a few
+    random term lists (suffix and prefix levels, direct children, several accumulators), for both
+    axis-view kinds."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_1403_3511_b200 import workloads as W
+
+    lib = nat.load(require_device=False)
+    cases = []
+    ap = W.CONFIGS["cfg3"].approx(0.0, validate=False)
+    cases.append((6, np.asarray(ap.degrees, dtype=np.int32), np.asarray(ap.coeffs, dtype=np.float64)))
+    gen = np.random.default_rng(5)
+    for dim in (2, 4, 8):
+        degs = gen.integers(0, 4, size=(24, dim))
+        degs[gen.random((24, dim)) < 0.6] = 0
+        degs = np.unique(degs, axis=0).astype(np.int32)
+        cases.append((dim, degs, gen.uniform(-1, 1, degs.shape[0])))
+    total = 0
+    for dim, degs, coeffs in cases:
+        degs = np.ascontiguousarray(degs)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        nk = C.c_int(0)
+        rc = lib.hp_level_jit_selftest(dim, degs.ctypes.data_as(nat.c_i32p), coeffs.ctypes.data_as(nat.c_dblp),
+                                       degs.shape[0], C.byref(nk))
+        assert rc == 0, lib.hp_last_error().decode()
+        assert nk.value >= 2
+        total += nk.value
+    assert total >= 8
