@@ -252,16 +252,17 @@ struct LvEnt {
   double w;
 };
 
-// One level as the kernel reads it (passed by value: constant bank).  Accumulated targets use a
-// DENSE weight table wt[(i * (K + 1) + k) * tgn + q] (zero where input i, degree k does not feed
-// target q), so the kernel's loops over degrees and targets are compile-time and an entry costs
-// one complex FMA with a uniform operand -- no per-entry decoding.  Child vectors with a single
-// term are written directly (`direct`), which keeps the accumulator count small.
+// a child vector with a single term: slot <- w T_k(X_a) input
 struct LvDirect {
   short slot;
   signed char k;
   double w;
 };
+// One level as the kernel reads it (passed by value: constant bank).  Accumulated targets use a
+// DENSE weight table wt[(i * (K + 1) + k) * tgn + q] (zero where input i, degree k does not feed
+// target q), so the kernel's loops over degrees and targets are compile-time and an entry costs
+// one complex FMA with a uniform operand -- no per-entry decoding.  Child vectors with a single
+// term are written directly (`direct`), which keeps the accumulator count small.
 struct LvLevel {
   int axis;
   int K;
