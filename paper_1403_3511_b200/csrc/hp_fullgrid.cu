@@ -113,7 +113,12 @@ struct FgPlan {
   // x1 x3 and x2 x4 (the halo boxes of k_fg_quad hold their taps; (1,2) and (2,3) corners are not staged)
   double cx02 = 0.0, cx13 = 0.0;
   bool extra() const { return cx02 != 0.0 || cx13 != 0.0; }
+  // the other T_1 (x) T_1 pairs -- (0,3), (1,2), (2,3) -- are added by a second, streaming pass
+  // (k_fg_pairs) after the fused evaluator: y += sum c_ab T_1(X_a) T_1(X_b) v
+  double cres[3] = {0.0, 0.0, 0.0};
+  bool residual() const { return cres[0] != 0.0 || cres[1] != 0.0 || cres[2] != 0.0; }
 };
+constexpr int FG_RES_A[3] = {0, 1, 2}, FG_RES_B[3] = {3, 2, 3};
 
 static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch, int flags) {
   FgPlan P;
@@ -148,6 +153,15 @@ static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dt
     if (na == 2 && t.r[act[0]] == 1 && t.r[act[1]] == 1 && act[0] == 1 && act[1] == 3) {
       P.cx13 += t.alpha;
       continue;
+    }
+    if (na == 2 && t.r[act[0]] == 1 && t.r[act[1]] == 1) {
+      bool placed = false;
+      for (int i = 0; i < 3; ++i)
+        if (act[0] == FG_RES_A[i] && act[1] == FG_RES_B[i]) {
+          P.cres[i] += t.alpha;
+          placed = true;
+        }
+      if (placed) continue;
     }
     return P;
   }
@@ -545,6 +559,8 @@ static bool fg_extra_ok(const hp_set_s* s, const FgPlan& F) {
   return !F.extra() || (fg_quad() && s->side[0] <= Q_MAXN && s->side[1] <= Q_MAXN && fg_single_class(F));
 }
 
+static hp_status launch_pairs(const hp_set_s* s, const FgPlan& F, const double2* v, double2* y, cudaStream_t st);
+
 hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                          const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
                          cudaStream_t st, bool* done, DotOut* dot, double sq) {
@@ -560,6 +576,7 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   const double2* v = (const double2*)in;
   double2* y = (double2*)out;
   const bool even = F.mask[0] == FG_MASK_EVEN && F.mask[2] == FG_MASK_EVEN && F.mask[3] == FG_MASK_EVEN;
+  if (F.residual()) dot = nullptr;  // <v, y> would miss the second pass: the caller forms it
   // single pass for the even-band class (cfg4); a batch runs one launch per vector
   if (fg_single_class(F) && fg_extra_ok(s, F)) {
     bool launched = false;
@@ -568,6 +585,7 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
       rc = launch_single_for(F, s, v + off, y + off, P, G, st, batch == 1 ? dot : nullptr, &launched);
       if (rc) return rc;
       if (!launched) break;
+      if ((rc = launch_pairs(s, F, v + off, y + off, st))) return rc;
     }
     if (launched) {
       *done = true;
@@ -595,10 +613,103 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   else
     rc = launch_outer<2, 2, FG_MASK_ALL, FG_MASK_ALL>(s, v, u, y, P, G, F, st, dot);
   if (rc) return rc;
+  if ((rc = launch_pairs(s, F, v, y, st))) return rc;
   *done = true;
   return HP_OK;
 }
 
+
+// ---------------------------------------------------------------- residual pair couplings
+
+struct PairArgs {
+  int side[4];
+  double c[3];  // coefficients of the pairs (0,3), (1,2), (2,3)
+};
+
+// y += sum_pairs c_ab T_1(X_a / L) T_1(X_b / L) v on a 4-D box: the four corner neighbours
+// (j_a +- 1, j_b +- 1) weighted by the T_1 bands (zero across the faces, global j on a slab's axis 0).
+// A streaming pass behind the fused evaluator for the pairs whose corners its halo boxes do not
+// hold (MASK: bit i = pair i present); blockIdx.y = j0, one thread per point of the plane,
+// consecutive threads along the last axis (32-bit index arithmetic inside the plane).
+template <int MASK>
+__global__ void __launch_bounds__(256) k_fg_pairs(const double2* __restrict__ v, double2* __restrict__ y,
+                                                  const double* __restrict__ basis, PairArgs A) {
+  constexpr size_t bs = (size_t)(FG_K + 1) * FG_MAXN * FG_W;
+  const unsigned n1 = A.side[1], n2 = A.side[2], n3 = A.side[3], plane = n1 * n2 * n3;
+  const int j0 = blockIdx.y;
+  const int64_t base = (int64_t)j0 * plane;
+  // T_1 band of axis a at row j: entries (j, j - 1) and (j, j + 1), zero across the faces
+  auto band = [&](int a, int j, double& wm, double& wp) {
+    const double* B = basis + a * bs + ((size_t)A.side[a] + j) * FG_W + FG_K;  // degree 1, row j, centre
+    wm = j > 0 ? __ldg(B - 1) : 0.0;
+    wp = j + 1 < A.side[a] ? __ldg(B + 1) : 0.0;
+  };
+  // c . sum over the corners (j_a +- 1, j_b +- 1); sa, sb = element strides of the two axes
+  auto corners = [&](const double2* x, int64_t sa, int64_t sb, double wam, double wap, double wbm, double wbp, double c,
+                     double2& acc) {
+    auto row = [&](const double2* xr, double wa) {
+      if (wa == 0.0) return;
+      double2 h = make_double2(0.0, 0.0);
+      if (wbm != 0.0) {
+        const double2 t = __ldg(xr - sb);
+        h.x = wbm * t.x;
+        h.y = wbm * t.y;
+      }
+      if (wbp != 0.0) {
+        const double2 t = __ldg(xr + sb);
+        h.x = fma(wbp, t.x, h.x);
+        h.y = fma(wbp, t.y, h.y);
+      }
+      acc.x = fma(c * wa, h.x, acc.x);
+      acc.y = fma(c * wa, h.y, acc.y);
+    };
+    row(x - sa, wam);
+    row(x + sa, wap);
+  };
+  double w0m = 0.0, w0p = 0.0;
+  if (MASK & 1) band(0, j0, w0m, w0p);
+  for (unsigned r = blockIdx.x * blockDim.x + threadIdx.x; r < plane; r += gridDim.x * blockDim.x) {
+    const unsigned j3 = r % n3, t = r / n3, j2 = t % n2, j1 = t / n2;
+    const double2* x = v + base + r;
+    double2 acc = make_double2(0.0, 0.0);
+    double w3m = 0.0, w3p = 0.0, w2m = 0.0, w2p = 0.0, w1m = 0.0, w1p = 0.0;
+    if (MASK & 5) band(3, (int)j3, w3m, w3p);
+    if (MASK & 6) band(2, (int)j2, w2m, w2p);
+    if (MASK & 2) band(1, (int)j1, w1m, w1p);
+    if (MASK & 1) corners(x, plane, 1, w0m, w0p, w3m, w3p, A.c[0], acc);
+    if (MASK & 2) corners(x, (int64_t)n2 * n3, n3, w1m, w1p, w2m, w2p, A.c[1], acc);
+    if (MASK & 4) corners(x, n3, 1, w2m, w2p, w3m, w3p, A.c[2], acc);
+    double2 out = y[base + r];
+    out.x += acc.x;
+    out.y += acc.y;
+    y[base + r] = out;
+  }
+}
+
+static hp_status launch_pairs(const hp_set_s* s, const FgPlan& F, const double2* v, double2* y, cudaStream_t st) {
+  if (!F.residual()) return HP_OK;
+  PairArgs A;
+  for (int a = 0; a < 4; ++a) A.side[a] = s->side[a];
+  int mask = 0;
+  for (int i = 0; i < 3; ++i) {
+    A.c[i] = F.cres[i];
+    if (F.cres[i] != 0.0) mask |= 1 << i;
+  }
+  const int64_t plane = (int64_t)s->side[1] * s->side[2] * s->side[3];
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((plane + 255) / 256, 8 * sm_count() / std::max(1, s->side[0]) + 1)),
+                  (unsigned)s->side[0]);
+  switch (mask) {
+    case 1: k_fg_pairs<1><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
+    case 2: k_fg_pairs<2><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
+    case 3: k_fg_pairs<3><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
+    case 4: k_fg_pairs<4><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
+    case 5: k_fg_pairs<5><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
+    case 6: k_fg_pairs<6><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
+    default: k_fg_pairs<7><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
+  }
+  HP_LAUNCH_CHECK("k_fg_pairs");
+  return HP_OK;
+}
 
 // ---------------------------------------------------------------- plane ranges
 
@@ -632,7 +743,7 @@ hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& term
                                 cudaStream_t st, bool* done, double* dot_accum, double sq) {
   *done = false;
   FgPlan F = classify(s, terms, dtype, 1, flags);
-  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F)) return HP_OK;
+  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F) || F.residual()) return HP_OK;
   if (plo == phi) {  // support query: nothing to compute
     *done = ws_bytes >= fullgrid_workspace_bytes(s, terms, dtype, 1, flags);
     return HP_OK;
@@ -693,7 +804,7 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
                                   void* ws, size_t ws_bytes, cudaStream_t st, bool* done) {
   *done = false;
   FgPlan F = classify(s, terms, dtype, 1, flags);
-  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F)) return HP_OK;
+  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F) || F.residual()) return HP_OK;
   bool ok = false;
   hp_status rc = fg_prepare(s, terms, halfwidth, dtype, 1, flags, ws, ws_bytes, st, &F, &ok);
   if (rc || !ok) return rc;

@@ -383,6 +383,46 @@ def test_fused_fullgrid_further_couplings(hp, rng, bound, cpl):
     assert rel_l2(y.cpu().numpy(), oa.hamiltonian(ap.degrees, ap.coeffs, 16.0, V[0])) < TOL
 
 
+@pytest.mark.parametrize("bound", [5, 11, 20])
+def test_fused_fullgrid_residual_pair_couplings(hp, rng, bound):
+    """Pair couplings whose corner taps the single-pass kernel does not stage (x1 x4, x2 x3,
+    x3 x4) are added by the streaming second pass k_fg_pairs behind it: a general quadratic
+    coupling matrix on N = 4 cubes and slabs against the oracle, and through the Lanczos loop
+    (which forms its own <v, A v> then)."""
+    from paper_1403_3511_b200.potential_approx import custom_potential, interpolate
+
+    cij = {(0, 1): 0.1, (0, 2): 0.07, (0, 3): -0.04, (1, 2): 0.06, (1, 3): 0.05, (2, 3): -0.03}
+
+    def w(p, t):
+        out = 0.5 * (p * p).sum(axis=-1) + 0.01 * (p ** 4).sum(axis=-1)
+        for (a, b), c in cij.items():
+            out = out + c * p[:, a] * p[:, b]
+        return out
+
+    spec = custom_potential(w, 4, 16.0)
+    ap = interpolate(spec, 4, 0.0)
+    side = bound + 1
+    s = hp.build_full(4, bound)
+    oa = O.applier_for_full(4, bound)
+    appl = hp.get_applier(s)
+    V = rng.standard_normal((2, s.size)) + 1j * rng.standard_normal((2, s.size))
+    Y = appl.apply_hamiltonian(ap, V)
+    for b in range(2):
+        assert rel_l2(Y[b], oa.hamiltonian(ap.degrees, ap.coeffs, 16.0, V[b])) < TOL
+    plane = side ** 3
+    for lo, hi in [(0, side // 2), (side // 3, side)]:
+        sl = hp.build_slab(4, bound, lo, hi)
+        ob = O.applier_for_slab(4, bound, lo, hi)
+        x = np.ascontiguousarray(V[1][lo * plane:hi * plane])
+        assert rel_l2(hp.get_applier(sl).apply_polynomial(ap, x), ob.polynomial(ap.degrees, ap.coeffs, 16.0, x)) < TOL
+    if bound == 11:
+        c = V[0] / np.linalg.norm(V[0])
+        fh = hp.FastHamiltonian(s, spec, 4)
+        got = hp.propagate_magnus(hp.MagnusScheme.from_name("midpoint"), fh.matvec_at, c, 0.0, 0.01, 2, 7)
+        want = O.propagate("midpoint", O.hamiltonian_at(oa, w, 4, 16.0, 4), c, 0.0, 0.01, 2, 7)
+        assert rel_l2(got, want) < TOL
+
+
 @pytest.mark.slow
 def test_cfg4_full_size_slab_vs_oracle(hp):
     """Full-size cfg4 (2.7e8 coefficients): GPU output on planes j1 in [62, 64) equals the oracle

@@ -26,7 +26,8 @@ y = torch.empty_like(x)
 appl = hp.get_applier(s)
 for name, w in (("cfg4-class (x1x2)", coupled(0.1, 0, 0)), ("x1x3", coupled(0, 0.1, 0)), ("x2x4", coupled(0, 0, 0.05)),
                 ("x1x3+x2x4", coupled(0, 0.1, 0.05)), ("x1x2+x1x3+x2x4", coupled(0.1, 0.1, 0.05)),
-                ("x2x3 (level evaluator)", coupled(0, 0, 0, 0.1))):
+                ("x2x3 (second pass k_fg_pairs)", coupled(0, 0, 0, 0.1)),
+                ("x1x2+x1x3+x2x4+x2x3", coupled(0.1, 0.1, 0.05, 0.1))):
     ap = interpolate(custom_potential(w, 4, 16.0), 4, 0.3, validate=False)
     for _ in range(2):
         appl.apply_into(ap, x, y)
