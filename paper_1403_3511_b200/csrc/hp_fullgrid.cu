@@ -629,15 +629,19 @@ struct PairArgs {
 // y += sum_pairs c_ab T_1(X_a / L) T_1(X_b / L) v on a 4-D box: the four corner neighbours
 // (j_a +- 1, j_b +- 1) weighted by the T_1 bands (zero across the faces, global j on a slab's axis 0).
 // A streaming pass behind the fused evaluator for the pairs whose corners its halo boxes do not
-// hold (MASK: bit i = pair i present); blockIdx.y = j0, one thread per point of the plane,
-// consecutive threads along the last axis (32-bit index arithmetic inside the plane).
+// hold (MASK: bit i = pair i present).  blockIdx.y = j0; a block owns 256 consecutive points of
+// the (j2, j3) cross-section and marches j1, so its j2 / j3 weights are formed once and the rows
+// (j1 + 1, j2 +- 1) it loads at one step are the rows (j1' - 1, ..) of the step after next
+// (L1 / L2 hits); consecutive threads run along the last axis.
 template <int MASK>
 __global__ void __launch_bounds__(256) k_fg_pairs(const double2* __restrict__ v, double2* __restrict__ y,
                                                   const double* __restrict__ basis, PairArgs A) {
   constexpr size_t bs = (size_t)(FG_K + 1) * FG_MAXN * FG_W;
-  const unsigned n1 = A.side[1], n2 = A.side[2], n3 = A.side[3], plane = n1 * n2 * n3;
-  const int j0 = blockIdx.y;
-  const int64_t base = (int64_t)j0 * plane;
+  const unsigned n1 = A.side[1], n2 = A.side[2], n3 = A.side[3], cross = n2 * n3;
+  const unsigned q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= cross) return;
+  const int j0 = blockIdx.y, j2 = (int)(q / n3), j3 = (int)(q % n3);
+  const int64_t plane = (int64_t)n1 * cross;
   // T_1 band of axis a at row j: entries (j, j - 1) and (j, j + 1), zero across the faces
   auto band = [&](int a, int j, double& wm, double& wp) {
     const double* B = basis + a * bs + ((size_t)A.side[a] + j) * FG_W + FG_K;  // degree 1, row j, centre
@@ -666,23 +670,25 @@ __global__ void __launch_bounds__(256) k_fg_pairs(const double2* __restrict__ v,
     row(x - sa, wam);
     row(x + sa, wap);
   };
-  double w0m = 0.0, w0p = 0.0;
+  double w0m = 0.0, w0p = 0.0, w3m = 0.0, w3p = 0.0, w2m = 0.0, w2p = 0.0;
   if (MASK & 1) band(0, j0, w0m, w0p);
-  for (unsigned r = blockIdx.x * blockDim.x + threadIdx.x; r < plane; r += gridDim.x * blockDim.x) {
-    const unsigned j3 = r % n3, t = r / n3, j2 = t % n2, j1 = t / n2;
-    const double2* x = v + base + r;
+  if (MASK & 5) band(3, j3, w3m, w3p);
+  if (MASK & 6) band(2, j2, w2m, w2p);
+  const double2* x = v + (int64_t)j0 * plane + q;
+  double2* yo = y + (int64_t)j0 * plane + q;
+  for (unsigned j1 = 0; j1 < n1; ++j1, x += cross, yo += cross) {
     double2 acc = make_double2(0.0, 0.0);
-    double w3m = 0.0, w3p = 0.0, w2m = 0.0, w2p = 0.0, w1m = 0.0, w1p = 0.0;
-    if (MASK & 5) band(3, (int)j3, w3m, w3p);
-    if (MASK & 6) band(2, (int)j2, w2m, w2p);
-    if (MASK & 2) band(1, (int)j1, w1m, w1p);
     if (MASK & 1) corners(x, plane, 1, w0m, w0p, w3m, w3p, A.c[0], acc);
-    if (MASK & 2) corners(x, (int64_t)n2 * n3, n3, w1m, w1p, w2m, w2p, A.c[1], acc);
+    if (MASK & 2) {
+      double w1m, w1p;
+      band(1, (int)j1, w1m, w1p);
+      corners(x, cross, n3, w1m, w1p, w2m, w2p, A.c[1], acc);
+    }
     if (MASK & 4) corners(x, n3, 1, w2m, w2p, w3m, w3p, A.c[2], acc);
-    double2 out = y[base + r];
+    double2 out = *yo;
     out.x += acc.x;
     out.y += acc.y;
-    y[base + r] = out;
+    *yo = out;
   }
 }
 
@@ -695,9 +701,7 @@ static hp_status launch_pairs(const hp_set_s* s, const FgPlan& F, const double2*
     A.c[i] = F.cres[i];
     if (F.cres[i] != 0.0) mask |= 1 << i;
   }
-  const int64_t plane = (int64_t)s->side[1] * s->side[2] * s->side[3];
-  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((plane + 255) / 256, 8 * sm_count() / std::max(1, s->side[0]) + 1)),
-                  (unsigned)s->side[0]);
+  const dim3 grid((unsigned)(((int64_t)s->side[2] * s->side[3] + 255) / 256), (unsigned)s->side[0]);
   switch (mask) {
     case 1: k_fg_pairs<1><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
     case 2: k_fg_pairs<2><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
