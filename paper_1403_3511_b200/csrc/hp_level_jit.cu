@@ -184,8 +184,11 @@ bool compile_cubin(const std::string& src, int minb, int* spills, std::vector<ch
   nvrtcProgram prog = nullptr;
   if (r.create(&prog, src.c_str(), "hp_level_gen.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return false;
   const std::string bounds = "-DLV_MINB=" + std::to_string(minb);
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--ptxas-options=-v", bounds.c_str()};
-  const nvrtcResult rc = r.compile(prog, 5, opts);
+  std::string extra = "-DHP_RTC=1";
+  if (const char* e = getenv("HP_LEVEL_JIT_DEFS")) extra = e;  // experiments: one more -D option
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--ptxas-options=-v", bounds.c_str(),
+                        extra.c_str()};
+  const nvrtcResult rc = r.compile(prog, 6, opts);
   size_t ls = 0;
   r.log_size(prog, &ls);
   std::string log(ls, '\0');
