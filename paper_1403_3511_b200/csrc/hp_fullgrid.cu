@@ -559,7 +559,8 @@ static bool fg_extra_ok(const hp_set_s* s, const FgPlan& F) {
   return !F.extra() || (fg_quad() && s->side[0] <= Q_MAXN && s->side[1] <= Q_MAXN && fg_single_class(F));
 }
 
-static hp_status launch_pairs(const hp_set_s* s, const FgPlan& F, const double2* v, double2* y, cudaStream_t st);
+static hp_status launch_pairs(const hp_set_s* s, const FgPlan& F, const double2* v, double2* y, cudaStream_t st,
+                              int plo = 0, int phi = -1);
 
 hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                          const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
@@ -635,12 +636,12 @@ struct PairArgs {
 // (L1 / L2 hits); consecutive threads run along the last axis.
 template <int MASK>
 __global__ void __launch_bounds__(256) k_fg_pairs(const double2* __restrict__ v, double2* __restrict__ y,
-                                                  const double* __restrict__ basis, PairArgs A) {
+                                                  const double* __restrict__ basis, PairArgs A, int plo) {
   constexpr size_t bs = (size_t)(FG_K + 1) * FG_MAXN * FG_W;
   const unsigned n1 = A.side[1], n2 = A.side[2], n3 = A.side[3], cross = n2 * n3;
   const unsigned q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= cross) return;
-  const int j0 = blockIdx.y, j2 = (int)(q / n3), j3 = (int)(q % n3);
+  const int j0 = plo + (int)blockIdx.y, j2 = (int)(q / n3), j3 = (int)(q % n3);  // output planes [plo, plo + gridDim.y)
   const int64_t plane = (int64_t)n1 * cross;
   // T_1 band of axis a at row j: entries (j, j - 1) and (j, j + 1), zero across the faces
   auto band = [&](int a, int j, double& wm, double& wp) {
@@ -692,8 +693,10 @@ __global__ void __launch_bounds__(256) k_fg_pairs(const double2* __restrict__ v,
   }
 }
 
-static hp_status launch_pairs(const hp_set_s* s, const FgPlan& F, const double2* v, double2* y, cudaStream_t st) {
-  if (!F.residual()) return HP_OK;
+static hp_status launch_pairs(const hp_set_s* s, const FgPlan& F, const double2* v, double2* y, cudaStream_t st,
+                              int plo, int phi) {
+  if (phi < 0) phi = s->side[0];
+  if (!F.residual() || phi <= plo) return HP_OK;
   PairArgs A;
   for (int a = 0; a < 4; ++a) A.side[a] = s->side[a];
   int mask = 0;
@@ -701,15 +704,15 @@ static hp_status launch_pairs(const hp_set_s* s, const FgPlan& F, const double2*
     A.c[i] = F.cres[i];
     if (F.cres[i] != 0.0) mask |= 1 << i;
   }
-  const dim3 grid((unsigned)(((int64_t)s->side[2] * s->side[3] + 255) / 256), (unsigned)s->side[0]);
+  const dim3 grid((unsigned)(((int64_t)s->side[2] * s->side[3] + 255) / 256), (unsigned)(phi - plo));
   switch (mask) {
-    case 1: k_fg_pairs<1><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
-    case 2: k_fg_pairs<2><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
-    case 3: k_fg_pairs<3><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
-    case 4: k_fg_pairs<4><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
-    case 5: k_fg_pairs<5><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
-    case 6: k_fg_pairs<6><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
-    default: k_fg_pairs<7><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A); break;
+    case 1: k_fg_pairs<1><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A, plo); break;
+    case 2: k_fg_pairs<2><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A, plo); break;
+    case 3: k_fg_pairs<3><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A, plo); break;
+    case 4: k_fg_pairs<4><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A, plo); break;
+    case 5: k_fg_pairs<5><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A, plo); break;
+    case 6: k_fg_pairs<6><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A, plo); break;
+    default: k_fg_pairs<7><<<grid, 256, 0, st>>>(v, y, s->fg_basis, A, plo); break;
   }
   HP_LAUNCH_CHECK("k_fg_pairs");
   return HP_OK;
@@ -747,7 +750,8 @@ hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& term
                                 cudaStream_t st, bool* done, double* dot_accum, double sq) {
   *done = false;
   FgPlan F = classify(s, terms, dtype, 1, flags);
-  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F) || F.residual()) return HP_OK;
+  // (with second-pass couplings the rows of x^H A x are not formed in-kernel: the caller's other route)
+  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F) || (F.residual() && dot_accum)) return HP_OK;
   if (plo == phi) {  // support query: nothing to compute
     *done = ws_bytes >= fullgrid_workspace_bytes(s, terms, dtype, 1, flags);
     return HP_OK;
@@ -771,6 +775,7 @@ hp_status fullgrid_apply_planes(const hp_set_s* s, const std::vector<Term>& term
     k_fg_dot_accum<<<1, 256, 0, st>>>(d.partial, d.n, dot_accum);
     HP_LAUNCH_CHECK("k_fg_dot_accum");
   }
+  if (launched && (rc = launch_pairs(s, F, (const double2*)in, (double2*)out, st, plo, phi))) return rc;
   *done = launched;
   return HP_OK;
 }
@@ -808,7 +813,7 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
                                   void* ws, size_t ws_bytes, cudaStream_t st, bool* done) {
   *done = false;
   FgPlan F = classify(s, terms, dtype, 1, flags);
-  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F) || F.residual()) return HP_OK;
+  if (!F.ok || !fg_single_class(F) || !fg_extra_ok(s, F)) return HP_OK;
   bool ok = false;
   hp_status rc = fg_prepare(s, terms, halfwidth, dtype, 1, flags, ws, ws_bytes, st, &F, &ok);
   if (rc || !ok) return rc;
@@ -844,6 +849,8 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
     rc = launch_single_for(F, s, (const double2*)in_dev, (double2*)out_dev, P, G, st, nullptr, &launched, p0, p1);
     if (rc) return rc;
     if (!launched) return fail(HP_ERR_RUNTIME, "streamed matvec: TMA descriptors unavailable");
+    // second-pass couplings of these planes: their corner rows (planes p0 - 1 .. p1) have arrived
+    if ((rc = launch_pairs(s, F, (const double2*)in_dev, (double2*)out_dev, st, p0, p1))) return rc;
     HP_CUDA(cudaEventRecord(ev[nch + k], st));
     HP_CUDA(cudaStreamWaitEvent(sout, ev[nch + k], 0));
     HP_CUDA(cudaMemcpyAsync((char*)out_host + p0 * plane, (const char*)out_dev + p0 * plane, (p1 - p0) * plane,

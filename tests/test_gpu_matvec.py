@@ -384,7 +384,7 @@ def test_fused_fullgrid_further_couplings(hp, rng, bound, cpl):
 
 
 @pytest.mark.parametrize("bound", [5, 11, 20])
-def test_fused_fullgrid_residual_pair_couplings(hp, rng, bound):
+def test_fused_fullgrid_residual_pair_couplings(hp, rng, bound, monkeypatch):
     """Pair couplings whose corner taps the single-pass kernel does not stage (x1 x4, x2 x3,
     x3 x4) are added by the streaming second pass k_fg_pairs behind it: a general quadratic
     coupling matrix on N = 4 cubes and slabs against the oracle, and through the Lanczos loop
@@ -415,6 +415,24 @@ def test_fused_fullgrid_residual_pair_couplings(hp, rng, bound):
         ob = O.applier_for_slab(4, bound, lo, hi)
         x = np.ascontiguousarray(V[1][lo * plane:hi * plane])
         assert rel_l2(hp.get_applier(sl).apply_polynomial(ap, x), ob.polynomial(ap.degrees, ap.coeffs, 16.0, x)) < TOL
+    # plane ranges (no fused dot) and the host-streamed entry point run the second pass per range / chunk
+    import torch
+
+    from paper_1403_3511_b200 import _native as nat
+
+    want = oa.hamiltonian(ap.degrees, ap.coeffs, 16.0, V[0])
+    x = torch.from_numpy(V[0]).cuda()
+    y = torch.empty_like(x)
+    cuts = [0, side // 3, side // 3 + 1, side]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        assert appl.apply_planes_into(ap, x, y, lo, hi, nat.HP_ADD_OSC)
+    assert rel_l2(y.cpu().numpy(), want) < TOL
+    monkeypatch.setenv("HP_STREAM_CHUNK", "3")
+    xh = torch.from_numpy(V[0]).pin_memory()
+    yh = torch.zeros_like(xh).pin_memory()
+    appl.apply_host_into(ap, xh, yh, nat.HP_ADD_OSC)
+    torch.cuda.synchronize()
+    assert rel_l2(yh.numpy(), want) < TOL
     if bound == 11:
         c = V[0] / np.linalg.norm(V[0])
         fh = hp.FastHamiltonian(s, spec, 4)
