@@ -619,7 +619,7 @@ hp_status hp_apply_polynomial(hp_set_t s, const int32_t* degrees, const double* 
   auto terms = make_terms(s->dim, degrees, coeffs, nterms);
   bool done = false;
   if (!(flags & HP_REF_ORDER) && !axis_order) {
-    rc = fullgrid_apply(s, terms, halfwidth, dtype, in, out, batch, flags, ws, ws_bytes, st, &done);
+    rc = fullgrid_apply_split(s, terms, halfwidth, dtype, in, out, batch, flags, ws, ws_bytes, st, &done);
     if (rc) return rc;
     if (!done) {
       rc = level_apply(s, terms, halfwidth, dtype, in, out, batch, flags, ws, ws_bytes, st, &done);

@@ -503,9 +503,27 @@ static hp_status launch_outer3(const hp_set_s* s, const double2* v, const double
   return HP_OK;
 }
 
+// the terms the fused evaluators take from any polynomial on an N = 4 box (constants, even
+// single-axis degrees, T_1 x T_1 pairs) and the rest, for fullgrid_apply_split
+static void split_fused_terms(const std::vector<Term>& terms, std::vector<Term>* fused, std::vector<Term>* rest) {
+  for (const Term& t : terms) {
+    int act[4], na = 0;
+    for (int a = 0; a < 4; ++a)
+      if (t.r[a] > 0) act[na++] = a;
+    const bool in_class = na == 0 || (na == 1 && t.r[act[0]] <= FG_K && t.r[act[0]] % 2 == 0) ||
+                          (na == 2 && t.r[act[0]] == 1 && t.r[act[1]] == 1);
+    (in_class ? fused : rest)->push_back(t);
+  }
+}
+
 size_t fullgrid_workspace_bytes(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch,
                                 int flags) {
   FgPlan F = classify(s, terms, dtype, batch, flags);
+  if (!F.ok && s->boxed && s->dim == 4) {  // room for the fused part of a split evaluation
+    std::vector<Term> fused, rest;
+    split_fused_terms(terms, &fused, &rest);
+    if (!fused.empty() && !rest.empty()) F = classify(s, fused, dtype, batch, flags);
+  }
   if (!F.ok) return 0;
   // bands | u (two-pass kernels) | per-CTA dot partials of the plane-range entry point
   return (size_t)FG_NTAB * FG_MAXN * FG_W * sizeof(double) + 256 + (size_t)s->n * sizeof(double2) + FG_DOTP_BYTES;
@@ -619,6 +637,35 @@ hp_status fullgrid_apply(const hp_set_s* s, const std::vector<Term>& terms, doub
   return HP_OK;
 }
 
+
+// ---------------------------------------------------------------- fused part + level remainder
+
+hp_status fullgrid_apply_split(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
+                               const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
+                               cudaStream_t st, bool* done, DotOut* dot, double sq) {
+  hp_status rc = fullgrid_apply(s, terms, halfwidth, dtype, in, out, batch, flags, ws, ws_bytes, st, done, dot, sq);
+  if (rc || *done) return rc;
+  if (!s->boxed || s->dim != 4 || dtype != HP_C128 || !fg_single_enabled()) return HP_OK;
+  std::vector<Term> fused, rest;
+  split_fused_terms(terms, &fused, &rest);
+  if (fused.empty() || rest.empty()) return HP_OK;
+  // the remainder must be cheaper in level passes than the whole polynomial by more than the fused launch
+  const double c_all = level_plan_cost(s->dim, terms), c_rest = level_plan_cost(s->dim, rest);
+  if (c_rest < 0.0 || (c_all >= 0.0 && c_rest + 2.0 > c_all)) return HP_OK;
+  if (level_workspace_bytes(s, rest, dtype, 1) > ws_bytes || fullgrid_workspace_bytes(s, fused, dtype, batch, flags) > ws_bytes ||
+      fullgrid_workspace_bytes(s, fused, dtype, batch, flags) == 0)
+    return HP_OK;
+  bool done_a = false, done_b = false;
+  rc = fullgrid_apply(s, fused, halfwidth, dtype, in, out, batch, flags, ws, ws_bytes, st, &done_a, nullptr, sq);
+  if (rc || !done_a) return rc;
+  // y += (remaining terms) v; the oscillator and the harmonic part went with the fused part
+  rc = level_apply(s, rest, halfwidth, dtype, in, out, batch, (flags & ~HP_ADD_OSC) | HP_LV_ACCUMULATE, ws, ws_bytes, st,
+                   &done_b, nullptr);
+  if (rc) return rc;
+  if (dot) dot->n = 0;  // <v, y> is left to the caller
+  *done = done_b;       // (not done: the caller's evaluator overwrites y with the whole polynomial)
+  return HP_OK;
+}
 
 // ---------------------------------------------------------------- residual pair couplings
 

@@ -547,8 +547,8 @@ static hp_status apply_ham(const Hamiltonian& H, const double2* v, double2* y, d
                            cudaStream_t st, DotOut* dot, bool* sq_done) {
   bool done = false;
   *sq_done = false;
-  hp_status rc = fullgrid_apply(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done,
-                                dot, H.q);
+  hp_status rc = fullgrid_apply_split(H.s, H.terms, H.halfwidth, HP_C128, v, y, 1, HP_ADD_OSC, ws, ws_bytes, st, &done,
+                                      dot, H.q);
   if (rc) return rc;
   if (done) {
     *sq_done = true;

@@ -649,6 +649,11 @@ static hp_status line_order(const hp_set_s* s, int a, cudaStream_t st, const int
 
 // ---------------------------------------------------------------- entry points
 
+double level_plan_cost(int dim, const std::vector<Term>& terms) {
+  const auto P = cached_plan(dim, terms);
+  return P->ok ? P->cost : -1.0;
+}
+
 size_t level_workspace_bytes(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch) {
   if (dtype != HP_C128) return 0;
   const auto Pp = cached_plan(s->dim, terms);
@@ -702,7 +707,7 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
     for (int li = 0; li < (int)P.levels.size(); ++li) {
       const LvLevel& lv = P.levels[li];
       const bool last = li == last_y;
-      const int first = li == first_y ? 1 : 0;
+      const int first = (li == first_y && !(flags & HP_LV_ACCUMULATE)) ? 1 : 0;
       double2* dotp = (last && dot && dot->partial && batch == 1 && grid <= dot->capacity) ? dot->partial : nullptr;
       const int32_t* perm = nullptr;
       hp_status rc = line_order(s, lv.axis, st, &perm);

@@ -86,7 +86,18 @@ hp_status fullgrid_apply_streamed(const hp_set_s* s, const std::vector<Term>& te
                                   const void* in_host, void* out_host, void* in_dev, void* out_dev, int flags,
                                   void* ws, size_t ws_bytes, cudaStream_t st, bool* done);
 
+// fullgrid_apply, and where the whole polynomial is outside the fused class of an N = 4 box: its
+// fused part (constants, even single-axis terms, T_1 x T_1 pairs) through the fused evaluator and
+// only the remaining terms through level passes accumulated onto y -- when the level planner
+// prices that below the whole polynomial
+hp_status fullgrid_apply_split(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
+                               const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,
+                               cudaStream_t st, bool* done, DotOut* dot = nullptr, double sq = 0.0);
+
 // level-fused evaluator (hp_level.cu): complex vectors, degrees <= 4
+constexpr int HP_LV_ACCUMULATE = 1 << 16;  // internal flag of level_apply: y += W v instead of y = W v
+// vector passes the level planner charges for the polynomial (< 0: not covered)
+double level_plan_cost(int dim, const std::vector<Term>& terms);
 size_t level_workspace_bytes(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch);
 hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double halfwidth, int dtype,
                       const void* in, void* out, int64_t batch, int flags, void* ws, size_t ws_bytes,

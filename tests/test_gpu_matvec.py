@@ -441,6 +441,42 @@ def test_fused_fullgrid_residual_pair_couplings(hp, rng, bound, monkeypatch):
         assert rel_l2(got, want) < TOL
 
 
+@pytest.mark.parametrize("bound", [7, 12])
+def test_fused_part_plus_level_remainder(hp, rng, bound):
+    """A polynomial outside the fused class on an N = 4 box (odd single-axis degrees, an x2^2 x3
+    term, a triple product) is evaluated as fused part + level passes accumulated onto y
+    (fullgrid_apply_split): cube, slab, batch, Hamiltonian, and two Magnus steps vs the oracle."""
+    from paper_1403_3511_b200.potential_approx import custom_potential, interpolate
+
+    def w(p, t):
+        return (0.5 * (p * p).sum(axis=-1) + 0.01 * (p ** 4).sum(axis=-1) + 0.1 * p[:, 0] * p[:, 1]
+                + 0.05 * p[:, 1] * p[:, 3] + 0.03 * p[:, 2] * p[:, 3] + 0.02 * p[:, 1] ** 2 * p[:, 2]
+                - 0.015 * p[:, 0] ** 3 + 0.01 * p[:, 0] * p[:, 2] * p[:, 3])
+
+    spec = custom_potential(w, 4, 16.0)
+    ap = interpolate(spec, 4, 0.0)
+    side = bound + 1
+    s = hp.build_full(4, bound)
+    oa = O.applier_for_full(4, bound)
+    appl = hp.get_applier(s)
+    V = rng.standard_normal((2, s.size)) + 1j * rng.standard_normal((2, s.size))
+    Y = appl.apply_polynomial(ap, V)
+    for b in range(2):
+        assert rel_l2(Y[b], oa.polynomial(ap.degrees, ap.coeffs, 16.0, V[b])) < TOL
+    assert rel_l2(appl.apply_hamiltonian(ap, V[0]), oa.hamiltonian(ap.degrees, ap.coeffs, 16.0, V[0])) < TOL
+    plane = side ** 3
+    lo, hi = 1, side - 2
+    sl = hp.build_slab(4, bound, lo, hi)
+    ob = O.applier_for_slab(4, bound, lo, hi)
+    x = np.ascontiguousarray(V[1][lo * plane:hi * plane])
+    assert rel_l2(hp.get_applier(sl).apply_hamiltonian(ap, x), ob.hamiltonian(ap.degrees, ap.coeffs, 16.0, x)) < TOL
+    c = V[0] / np.linalg.norm(V[0])
+    fh = hp.FastHamiltonian(s, spec, 4)
+    got = hp.propagate_magnus(hp.MagnusScheme.from_name("midpoint"), fh.matvec_at, c, 0.0, 0.01, 2, 7)
+    want = O.propagate("midpoint", O.hamiltonian_at(oa, w, 4, 16.0, 4), c, 0.0, 0.01, 2, 7)
+    assert rel_l2(got, want) < TOL
+
+
 @pytest.mark.slow
 def test_cfg4_full_size_slab_vs_oracle(hp):
     """Full-size cfg4 (2.7e8 coefficients): GPU output on planes j1 in [62, 64) equals the oracle

@@ -19,6 +19,10 @@ def coupled(c01, c02, c13, c12=0.0):
     return w
 
 
+def w_split(p, t):  # outside the fused class: x2^2 x3 and x1^3 go through level passes onto the fused part
+    return coupled(0.1, 0.0, 0.05)(p, t) + 0.02 * p[:, 1] ** 2 * p[:, 2] - 0.015 * p[:, 0] ** 3
+
+
 s = hp.build_full(4, bound)
 n = s.size
 x = torch.randn(n, dtype=torch.complex128, device="cuda")
@@ -27,7 +31,8 @@ appl = hp.get_applier(s)
 for name, w in (("cfg4-class (x1x2)", coupled(0.1, 0, 0)), ("x1x3", coupled(0, 0.1, 0)), ("x2x4", coupled(0, 0, 0.05)),
                 ("x1x3+x2x4", coupled(0, 0.1, 0.05)), ("x1x2+x1x3+x2x4", coupled(0.1, 0.1, 0.05)),
                 ("x2x3 (second pass k_fg_pairs)", coupled(0, 0, 0, 0.1)),
-                ("x1x2+x1x3+x2x4+x2x3", coupled(0.1, 0.1, 0.05, 0.1))):
+                ("x1x2+x1x3+x2x4+x2x3", coupled(0.1, 0.1, 0.05, 0.1)),
+                ("x1x2+x2x4+x2^2x3+x1^3 (fused part + level remainder)", w_split)):
     ap = interpolate(custom_potential(w, 4, 16.0), 4, 0.3, validate=False)
     for _ in range(2):
         appl.apply_into(ap, x, y)
