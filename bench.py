@@ -470,6 +470,7 @@ def gpu_arm(args, rank, world, local_rank):
                            ("single" if world == 1 else f"batch/{world}" if part else f"replicas x{world}")},
                 "roofline": roofline, "fp64": fp64_utilisation(w.name, ms_step) if not emu and world == 1 else None,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "specialised_level_kernels": int(nat.lib().hp_level_jit_kernels()),
                 "clocks": clk.summary(), "propagation": prop}
         print(json.dumps(line), flush=True)
 
@@ -571,7 +572,8 @@ def propagation_leg(args, w, rank, world, local_rank, hbm, peak_kind, sharded):
                         "frac": round(achieved / hbm, 4), "peak_kind": peak_kind,
                         "algorithmic_bytes_per_step": alg,
                         "basis": f"(112 m - 48) B per coefficient-step at m = {m} (SURVEY §8(d)), per GPU"},
-           "gpu_launches": int(launches), "clocks": clk.summary(),
+           "gpu_launches": int(launches), "specialised_level_kernels": int(nat.lib().hp_level_jit_kernels()),
+           "clocks": clk.summary(),
            "parallelism": f"slab-j1 x{world}" if sharded else ("single" if world == 1 else f"replicas x{world}")}
     if world == 1 and not sharded and not args.no_e2e:
         # e2e: propagate_magnus on a pinned host state (a CPU torch tensor in, a CPU tensor out):

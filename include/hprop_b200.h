@@ -67,6 +67,9 @@ int64_t hp_launch_count(void);
  * boxed); *nkernels_out = kernels compiled.  HP_ERR_RUNTIME if NVRTC is unavailable or a
  * compilation fails.  The build check of the path hp_apply_polynomial takes on large sets
  * (fast_apply.py:110-164; csrc/hp_level_jit.cu). */
+/* level kernels this process has compiled at run time so far (0: every level ran the library's
+ * interpreted kernel) */
+int hp_level_jit_kernels(void);
 hp_status hp_level_jit_selftest(int dim, const int32_t* degrees, const double* coeffs, int nterms,
                                 int* nkernels_out);
 

@@ -39,6 +39,7 @@ SIGNATURES = {
     "hp_last_error": (ctypes.c_char_p, []),
     "hp_device_count": (c_int, []),
     "hp_launch_count": (c_i64, []),
+    "hp_level_jit_kernels": (c_int, []),
     "hp_level_jit_selftest": (c_int, [c_int, c_i32p, c_dblp, c_int, ctypes.POINTER(c_int)]),
     "hp_set_create_full": (c_int, [c_int, c_int, c_vp, ctypes.POINTER(c_vp), c_i64p]),
     "hp_set_create_slab": (c_int, [c_int, c_int, c_int, c_int, c_vp, ctypes.POINTER(c_vp), c_i64p]),

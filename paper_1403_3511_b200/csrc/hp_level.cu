@@ -445,6 +445,7 @@ bool level_jit_launch(int device, const char* ax_name, const void* ax, const cha
                       const int32_t* perm, const double* sqtab);
 
 bool level_jit_compile_only(const LvLevel& lv, const char* ax_name, const char* axs_name);
+int level_jit_compiled();
 
 // the specialised kernel of a large level if there is one, else the instantiation whose accumulator
 // count matches the level's dense weight table
@@ -729,6 +730,8 @@ hp_status level_apply(const hp_set_s* s, const std::vector<Term>& terms, double 
 }
 
 }  // namespace hp
+
+extern "C" int hp_level_jit_kernels(void) { return hp::level_jit_compiled(); }
 
 extern "C" hp_status hp_level_jit_selftest(int dim, const int32_t* degrees, const double* coeffs, int nterms,
                                            int* nkernels_out) {

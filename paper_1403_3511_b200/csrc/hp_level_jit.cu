@@ -14,6 +14,7 @@
 #include <nvrtc.h>
 #include <cuda.h>
 
+#include <atomic>
 #include <cctype>
 #include <cstdlib>
 #include <cstring>
@@ -233,7 +234,11 @@ CUfunction compile_kernel(const std::string& src) {
   return fn;
 }
 
+std::atomic<int> g_compiled{0};
+
 }  // namespace
+
+int level_jit_compiled() { return g_compiled.load(); }
 
 // compiles one level for the given axis views without loading it (no device needed)
 bool level_jit_compile_only(const LvLevel& lv, const char* ax_name, const char* axs_name) {
@@ -285,6 +290,7 @@ bool level_jit_launch(int device, const char* ax_name, const void* ax, const cha
         }
       }
       fn = compile_kernel(src);
+      if (fn) ++g_compiled;
       if (debug_on())
         fprintf(stderr, "[hp_level_jit] axis %d K %d: %s (%zu weights)\n", lv.axis, lv.K, fn ? "compiled" : "FAILED",
                 w.size());
