@@ -1,4 +1,6 @@
-// Runtime specialisation of the level kernel (hp_device.cuh lv_body) for one level's structure.
+// Runtime specialisation of the level kernel (hp_device.cuh lv_body) for one level's structure:
+// part of the default evaluator of PolynomialApplier.apply_polynomial (fast_apply.py:110-164; the
+// recurrences of :69-92 as band rows) on reduced sets and on full cubes outside the fused class.
 //
 // The library's k_level interprets an LvLevel: per ordinal and input vector it decodes masks,
 // buffer numbers and a dense weight table from the constant bank, which is ~half of its issued
