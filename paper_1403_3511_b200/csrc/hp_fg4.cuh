@@ -4,7 +4,8 @@
 //   y = [c0 + sum_a P_a(X_a) + T_r0(X_0) G(X_1)] v  on a 4-D box (axes 0-based, axis 0 = j1),
 // one read of v and one write of y per coefficient.  MIX selects the couplings: bit 0 the
 // (0,1) class above; bit 1 adds c02 T_1(X_0) T_1(X_2) (x1 x3: its axis-2 taps b +- 1 come from
-// A1 / the B2 boxes and join the same march-axis scatter); bit 3 adds c13 T_1(X_1) T_1(X_3)
+// A1 / the B2 boxes and join the same march-axis scatter); bit 2 adds c03 T_1(X_0) T_1(X_3) (x1 x4:
+// taps c +- 1 of the same rows, same scatter); bit 3 adds c13 T_1(X_1) T_1(X_3)
 // (x2 x4: an in-plane term whose corner taps (a +- 1, c +- 1) lie inside box A1).  The other
 // pairs' corners are not staged.  What changes against k_fg_single is the per-SM working set:
 //
@@ -36,7 +37,7 @@
 // (the instantiation with all three couplings keeps them: its live ranges spill otherwise)
 #define Q_FENCE()                                                   \
   do {                                                              \
-    if (Q_FENCES || MIX == 11) asm volatile("" ::: "memory"); \
+    if (Q_FENCES || MIX == 11 || MIX == 15) asm volatile("" ::: "memory"); \
   } while (0)
 
 namespace hp {
@@ -63,8 +64,8 @@ constexpr int Q_T1W = 8;  // doubles per axis-1 weight row
 constexpr size_t Q_TOFF = Q_WOFF + (size_t)Q_MAXN * F1_WROW * sizeof(double);
 constexpr size_t Q_T2OFF = Q_TOFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
 constexpr size_t Q_T3OFF = Q_T2OFF + (size_t)(Q_MAXN + 8) * Q_T1W * sizeof(double);
-constexpr int Q_T3N = Q_MAXN + 16;  // axis-3 table: [5][Q_T3N], transposed (16 lanes read 128 B)
-constexpr int Q_T3ROWS = 7;  // P3(-4, -2, 2, 4, 0) and B_{3,1}(-1, +1) (MIX & 8)
+constexpr int Q_T3N = Q_MAXN;  // axis-3 table: [Q_T3ROWS][Q_T3N], transposed (16 lanes read 128 B); J3 < ceil(n3 / 16) * 16 <= Q_MAXN
+constexpr int Q_T3ROWS = 9;  // P3(-4, -2, 2, 4, 0), B_{3,1}(-1, +1) (MIX & 8), c03 B_{3,1}(-1, +1) (MIX & 4)
 constexpr size_t Q_BOFF = Q_T3OFF + (size_t)Q_T3ROWS * Q_T3N * sizeof(double);
 constexpr int Q_TC = 64;  // tile codes cached in shared memory
 constexpr size_t Q_SMEM = Q_BOFF + 2 * Q_S * sizeof(uint64_t) + (Q_S + Q_TC) * sizeof(int);
@@ -158,6 +159,10 @@ __global__ void __launch_bounds__(Q_NT, 1)
     if (MIX & 8) {
       T3w[5 * Q_T3N + r] = ok ? G[(size_t)4 * FG_MAXN * FG_W + r * FG_W + FG_K - 1] : 0.0;  // B_{3,1}(r, -1)
       T3w[6 * Q_T3N + r] = ok ? G[(size_t)4 * FG_MAXN * FG_W + r * FG_W + FG_K + 1] : 0.0;  // B_{3,1}(r, +1)
+    }
+    if (MIX & 4) {
+      T3w[7 * Q_T3N + r] = ok ? G[(size_t)5 * FG_MAXN * FG_W + r * FG_W + FG_K - 1] : 0.0;  // c03 B_{3,1}(r, -1)
+      T3w[8 * Q_T3N + r] = ok ? G[(size_t)5 * FG_MAXN * FG_W + r * FG_W + FG_K + 1] : 0.0;  // c03 B_{3,1}(r, +1)
     }
   }
   __syncthreads();
@@ -331,9 +336,9 @@ __global__ void __launch_bounds__(Q_NT, 1)
             fma2(wb23.y, t3, rb);
             Q_FENCE();
           }
-          // phase C: couplings through the march axis, g = [G(X_1) + c02 T_1(X_2)] v at rows a, a+2,
+          // phase C: couplings through the march axis, g = [G(X_1) + c02 T_1(X_2) + c03 T_1(X_3)] v at rows a, a+2,
           // scattered through T_r0(X_0) to y(p +- 1)
-          if (MIX & 3) {
+          if (MIX & 7) {
             const double2 ga = make_double2(QT1A(4), QT1A(5)), gb = make_double2(QT1B(4), QT1B(5));
             const double2 wcd = make_double2(wc.y, wd);
 #pragma unroll
@@ -360,6 +365,13 @@ __global__ void __launch_bounds__(Q_NT, 1)
                 fma2(cp, st[op], g);
                 fma2(cm, st[om + dm], g2);
                 fma2(cp, st[op + dp], g2);
+              }
+              if (MIX & 4) {  // axis-3 taps c -+ 1 of the same rows
+                const double em = Q3(7), ep = Q3(8);
+                fma2(em, st[o - 1], g);
+                fma2(ep, st[o + 1], g);
+                fma2(em, st[o + 2 * Q_R1 - 1], g2);
+                fma2(ep, st[o + 2 * Q_R1 + 1], g2);
               }
               fma2(wcd.x, g, Ra[(U + 1) & 7]);
               fma2(wcd.y, g, Ra[(U + 7) & 7]);

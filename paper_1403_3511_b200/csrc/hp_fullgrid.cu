@@ -109,16 +109,16 @@ struct FgPlan {
   unsigned mask[4] = {0, 0, 0, 0}; // nonzero diagonals of the combined single-axis bands
   unsigned maskG = 0;              // nonzero diagonals of the mixed-term axis-2 bands G_m
   bool twopass = true;             // the cube fits the two-pass kernels' chunking (single pass: any side)
-  // further T_1 (x) T_1 couplings of the single-pass quad kernel: axes (0,2) and (1,3), i.e.
-  // x1 x3 and x2 x4 (the halo boxes of k_fg_quad hold their taps; (1,2) and (2,3) corners are not staged)
-  double cx02 = 0.0, cx13 = 0.0;
-  bool extra() const { return cx02 != 0.0 || cx13 != 0.0; }
-  // the other T_1 (x) T_1 pairs -- (0,3), (1,2), (2,3) -- are added by a second, streaming pass
+  // further T_1 (x) T_1 couplings of the single-pass quad kernel: axes (0,2), (0,3) and (1,3), i.e.
+  // x1 x3, x1 x4 and x2 x4 (the halo boxes of k_fg_quad hold their taps; (1,2) and (2,3) corners are not staged)
+  double cx02 = 0.0, cx03 = 0.0, cx13 = 0.0;
+  bool extra() const { return cx02 != 0.0 || cx03 != 0.0 || cx13 != 0.0; }
+  // the other T_1 (x) T_1 pairs -- (1,2), (2,3) -- are added by a second, streaming pass
   // (k_fg_pairs) after the fused evaluator: y += sum c_ab T_1(X_a) T_1(X_b) v
   double cres[3] = {0.0, 0.0, 0.0};
   bool residual() const { return cres[0] != 0.0 || cres[1] != 0.0 || cres[2] != 0.0; }
 };
-constexpr int FG_RES_A[3] = {0, 1, 2}, FG_RES_B[3] = {3, 2, 3};
+constexpr int FG_RES_A[3] = {-1, 1, 2}, FG_RES_B[3] = {-1, 2, 3};  // (slot 0: x1 x4, now inside k_fg_quad)
 
 static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dtype, int64_t batch, int flags) {
   FgPlan P;
@@ -154,6 +154,10 @@ static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dt
       P.cx13 += t.alpha;
       continue;
     }
+    if (na == 2 && t.r[act[0]] == 1 && t.r[act[1]] == 1 && act[0] == 0 && act[1] == 3) {
+      P.cx03 += t.alpha;
+      continue;
+    }
     if (na == 2 && t.r[act[0]] == 1 && t.r[act[1]] == 1) {
       bool placed = false;
       for (int i = 0; i < 3; ++i)
@@ -187,13 +191,13 @@ static FgPlan classify(const hp_set_s* s, const std::vector<Term>& terms, int dt
 
 // ---------------------------------------------------------------- kernels
 
-// band tables in the workspace: P[4] | G[2] (mixed classes of axes (0,1)) | cx02 B_{2,1} | cx13 B_{1,1} | B_{3,1}
-constexpr int FG_NTAB = 9;
+// band tables in the workspace: P[4] | G[2] (mixed classes of axes (0,1)) | cx02 B_{2,1} | cx13 B_{1,1} | B_{3,1} | cx03 B_{3,1}
+constexpr int FG_NTAB = 10;
 
 struct CombineArgs {
   double ws[4][FG_K + 1];
   double wm[2][FG_K + 1];
-  double cx02, cx13;
+  double cx02, cx03, cx13;
   int side[4];
   int joff0;
   int nmix;
@@ -243,7 +247,7 @@ __global__ void k_fg_combine(const double* __restrict__ basis, double* __restric
     } else {
       // T_1 bands of the further couplings: cx02 B_{2,1}, cx13 B_{1,1}, B_{3,1}
       const int a = tab == 6 ? 2 : (tab == 7 ? 1 : 3);
-      const double c = tab == 6 ? A.cx02 : (tab == 7 ? A.cx13 : 1.0);
+      const double c = tab == 6 ? A.cx02 : (tab == 7 ? A.cx13 : (tab == 8 ? 1.0 : A.cx03));
       const int n = A.side[a];
       G[(size_t)(tab - 4) * FG_MAXN * FG_W + rem] = (j < n && c != 0.0) ? c * basis[a * bs + ((size_t)1 * n + j) * FG_W + d] : 0.0;
     }
@@ -362,7 +366,7 @@ static int sm_count() {
 }
 
 // k_fg_quad: 8 x 8 x 16 tiles, sides <= Q_MAXN
-// MIX: bit 0 = the (0,1) coupling class, bit 1 = (0,2), bit 3 = (1,3) (hp_fg4.cuh)
+// MIX: bit 0 = the (0,1) coupling class, bit 1 = (0,2), bit 2 = (0,3), bit 3 = (1,3) (hp_fg4.cuh)
 constexpr int FG_MIX_ALL = 1 | 2 | 8;
 template <int NMIX>
 static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, const double* P, const double* G,
@@ -379,8 +383,8 @@ static hp_status launch_quad(const hp_set_s* s, const double2* v, double2* y, co
   const bool use_dot = dot && dot->partial && grid <= dot->capacity;
   double2* dotp = use_dot ? dot->partial : nullptr;
   auto kern = use_dot ? k_fg_quad<NMIX, true> : k_fg_quad<NMIX, false>;
-  if (NMIX == FG_MIX_ALL && !use_dot && grid <= FG_DOTP) {
-    // all three couplings: ptxas spills the plain instantiation inside the march (152 bytes of
+  if ((NMIX == 7 || NMIX == FG_MIX_ALL || NMIX == 15) && !use_dot && grid <= FG_DOTP) {
+    // three or more couplings: ptxas spills the plain instantiation inside the march (152 bytes of
     // reloads per step, 4.9 ms on the cfg4 cube) but not the one with the fused dot, so that one
     // runs, its partials going to the workspace's dot region (behind the tables and the u vector)
     kern = k_fg_quad<NMIX, true>;
@@ -437,7 +441,8 @@ static hp_status launch_single_for(const FgPlan& F, const hp_set_s* s, const dou
                                    const double* G, cudaStream_t st, DotOut* dot, bool* launched, int plo = 0,
                                    int phi = -1) {
   // one instantiation per set of couplings present (an absent coupling costs no shared-memory taps)
-  const int mix = (F.nmix ? 1 : 0) | (F.cx02 != 0.0 ? 2 : 0) | (F.cx13 != 0.0 ? 8 : 0);
+  int mix = (F.nmix ? 1 : 0) | (F.cx02 != 0.0 ? 2 : 0) | (F.cx13 != 0.0 ? 8 : 0);
+  if (F.cx03 != 0.0) mix |= 7;  // x1 x4 comes with the whole march-axis family (two more instantiations, not eight)
   switch (mix) {
     case 0: return launch_single<0>(s, v, y, P, G, F, st, dot, launched, plo, phi);
     case 1: return launch_single<1>(s, v, y, P, G, F, st, dot, launched, plo, phi);
@@ -446,6 +451,8 @@ static hp_status launch_single_for(const FgPlan& F, const hp_set_s* s, const dou
     case 8: return launch_single<8>(s, v, y, P, G, F, st, dot, launched, plo, phi);
     case 9: return launch_single<9>(s, v, y, P, G, F, st, dot, launched, plo, phi);
     case 10: return launch_single<10>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+    case 7: return launch_single<7>(s, v, y, P, G, F, st, dot, launched, plo, phi);
+    case 15: return launch_single<15>(s, v, y, P, G, F, st, dot, launched, plo, phi);
     default: return launch_single<FG_MIX_ALL>(s, v, y, P, G, F, st, dot, launched, plo, phi);
   }
 }
@@ -555,6 +562,7 @@ static hp_status fg_prepare(const hp_set_s* s, const std::vector<Term>& terms, d
   A.joff0 = s->lo;
   A.nmix = F.nmix;
   A.cx02 = F.cx02;
+  A.cx03 = F.cx03;
   A.cx13 = F.cx13;
   A.c0 = F.c0;
   A.osc = (flags & HP_ADD_OSC) ? 1 : 0;

@@ -336,15 +336,16 @@ def test_fused_fullgrid_sizes_and_slabs(hp, bound):
         assert rel_l2(hp.get_applier(sl).apply_hamiltonian(ap, x), ob.hamiltonian(ap.degrees, ap.coeffs, 16.0, x)) < TOL
 
 
-def _coupled_potential(c01, c02, c13):
-    """cfg4's potential with further pair couplings: x1 x2 (c01), x1 x3 (c02), x2 x4 (c13)."""
+def _coupled_potential(c01, c02, c13, c03=0.0):
+    """cfg4's potential with further pair couplings: x1 x2 (c01), x1 x3 (c02), x2 x4 (c13), x1 x4 (c03)."""
     def w(p, t):
         return (0.5 * (p * p).sum(axis=-1) + c01 * math.cos(2.0 * t) * p[:, 0] * p[:, 1] + c02 * p[:, 0] * p[:, 2]
-                + c13 * p[:, 1] * p[:, 3] + 0.01 * (p ** 4).sum(axis=-1))
+                + c13 * p[:, 1] * p[:, 3] + c03 * p[:, 0] * p[:, 3] + 0.01 * (p ** 4).sum(axis=-1))
     return w
 
 
-@pytest.mark.parametrize("cpl", [(0.0, 0.07, 0.0), (0.0, 0.0, 0.05), (0.1, 0.07, 0.05)], ids=["x1x3", "x2x4", "all"])
+@pytest.mark.parametrize("cpl", [(0.0, 0.07, 0.0), (0.0, 0.0, 0.05), (0.1, 0.07, 0.05), (0.0, 0.0, 0.0, -0.06),
+                                 (0.1, 0.07, 0.05, -0.06)], ids=["x1x3", "x2x4", "all", "x1x4", "all4"])
 @pytest.mark.parametrize("bound", [5, 11, 20])
 def test_fused_fullgrid_further_couplings(hp, rng, bound, cpl):
     """The single-pass quad kernel's wider class (k_fg_quad<MIX>: x1 x3 through the march-axis

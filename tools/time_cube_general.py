@@ -12,10 +12,10 @@ bound = int(sys.argv[1]) if len(sys.argv) > 1 else 127
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 
 
-def coupled(c01, c02, c13, c12=0.0):
+def coupled(c01, c02, c13, c12=0.0, c03=0.0):
     def w(p, t):
         return (0.5 * (p * p).sum(axis=-1) + c01 * math.cos(2.0 * t) * p[:, 0] * p[:, 1] + c02 * p[:, 0] * p[:, 2]
-                + c13 * p[:, 1] * p[:, 3] + c12 * p[:, 1] * p[:, 2] + 0.01 * (p ** 4).sum(axis=-1))
+                + c13 * p[:, 1] * p[:, 3] + c12 * p[:, 1] * p[:, 2] + c03 * p[:, 0] * p[:, 3] + 0.01 * (p ** 4).sum(axis=-1))
     return w
 
 
@@ -29,9 +29,10 @@ x = torch.randn(n, dtype=torch.complex128, device="cuda")
 y = torch.empty_like(x)
 appl = hp.get_applier(s)
 for name, w in (("cfg4-class (x1x2)", coupled(0.1, 0, 0)), ("x1x3", coupled(0, 0.1, 0)), ("x2x4", coupled(0, 0, 0.05)),
-                ("x1x3+x2x4", coupled(0, 0.1, 0.05)), ("x1x2+x1x3+x2x4", coupled(0.1, 0.1, 0.05)),
+                ("x1x4", coupled(0, 0, 0, 0, -0.06)), ("x1x3+x2x4", coupled(0, 0.1, 0.05)), ("x1x2+x1x3+x2x4", coupled(0.1, 0.1, 0.05)),
                 ("x2x3 (second pass k_fg_pairs)", coupled(0, 0, 0, 0.1)),
                 ("x1x2+x1x3+x2x4+x2x3", coupled(0.1, 0.1, 0.05, 0.1)),
+                ("all six pairs", coupled(0.1, 0.1, 0.05, 0.1, -0.06)),
                 ("x1x2+x2x4+x2^2x3+x1^3 (fused part + level remainder)", w_split)):
     ap = interpolate(custom_potential(w, 4, 16.0), 4, 0.3, validate=False)
     for _ in range(2):
