@@ -146,6 +146,16 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut,
   std::vector<Node> nodes{{BUF_V_, {}}};
   bool y_written = false;
   double cost = 0.0;
+  // y entries moved from the first y level to the level after it (see below): (buffer, weight) of T_0 entries
+  std::vector<std::pair<int, double>> deferred;
+  static const bool defer_enabled = [] {
+    const char* e = getenv("HP_LEVEL_DEFER");
+    return !e || atoi(e) != 0;
+  }();
+  auto flush_deferred = [&](Builder& B) {
+    for (auto& d : deferred) B.add(BUF_Y_, d.first, 0, d.second);
+    deferred.clear();
+  };
   // terms with all degrees zero: harvested at the first level
   std::vector<int> consts;
   for (size_t i = 0; i < terms.size(); ++i) {
@@ -158,6 +168,7 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut,
     std::vector<int> inputs;
     for (auto& nd : nodes) if (nd.buf >= 0) inputs.push_back(nd.buf);
     if (!y_written) for (int it : consts) B.add(BUF_Y_, BUF_V_, 0, terms[it].alpha);
+    flush_deferred(B);
     // candidate next nodes: T_k(X_a) u_parent (k > 0: a new vector) or u_parent itself (k = 0)
     struct Cand {
       int parent, k;
@@ -230,6 +241,40 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut,
       for (auto& mem : gr.members) B.add(sl, cands[mem.first].parent, cands[mem.first].k, mem.second);
       next.push_back({sl, rep.rows});
     }
+    // The first level that writes y does not have to: a T_0 entry on v, and an entry that equals a
+    // single-term child vector of this level up to a factor, are the same numbers at the next
+    // level, which reads v and that child anyway -- y is then first written there, and this level
+    // neither writes nor the next one re-reads it (cfg3: 32 of 500 B per coefficient).
+    if (defer_enabled && !y_written && B.tg.count(BUF_Y_)) {
+      std::vector<std::pair<int, double>> moved;
+      bool all = true;
+      for (auto& oe : B.tg[BUF_Y_]) {
+        const LvEnt& e = oe.second;
+        if (e.k == 0) {
+          if (B.L.in_buf[e.input] != BUF_V_) { all = false; break; }
+          moved.push_back({BUF_V_, e.w});
+          continue;
+        }
+        bool found = false;
+        for (auto& t : B.tg) {
+          if (t.first < 0 || t.second.size() != 1) continue;
+          const LvEnt& c = t.second[0].second;
+          bool is_node = false;
+          for (auto& nd : next) is_node |= nd.buf == t.first;
+          if (is_node && c.input == e.input && c.k == e.k && c.w != 0.0) {
+            moved.push_back({t.first, e.w / c.w});
+            found = true;
+            break;
+          }
+        }
+        if (!found) { all = false; break; }
+      }
+      if (all) {
+        B.tg.erase(BUF_Y_);
+        deferred = moved;
+        y_written = true;  // the constants travel with the deferred entries
+      }
+    }
     std::vector<int> released;
     for (int buf : inputs) {
       bool live = false;
@@ -254,6 +299,7 @@ static LvProgram plan_with_cut(int dim, const std::vector<Term>& terms, int cut,
     std::vector<int> inputs;
     for (auto& nd : nodes) if (nd.buf >= 0) inputs.push_back(nd.buf);
     if (!y_written) for (int it : consts) B.add(BUF_Y_, BUF_V_, 0, terms[it].alpha);
+    flush_deferred(B);
     for (auto& nd : nodes) {
       for (int it : nd.rows) {
         const Term& t = terms[it];
