@@ -180,6 +180,43 @@ def test_sharded_propagation_emulated(bound, world, q):
     assert float(torch.linalg.vector_norm(got - want) / torch.linalg.vector_norm(want)) < 1e-12
 
 
+def test_sharded_propagation_general_couplings():
+    """The sharded Magnus loop with a potential whose pair couplings need the second pass (so the
+    plane entry point cannot supply the in-kernel dot: whole-box matvec + separate reductions)
+    against the single-device propagation: 2 steps, 3 emulated ranks."""
+    import torch
+
+    import paper_1403_3511_b200 as hp
+    from paper_1403_3511_b200 import workloads as W
+    from paper_1403_3511_b200.sharding import SlabShard, emulate_exchange, local_sum, sharded_propagate
+
+    cij = {(0, 1): 0.1, (0, 2): 0.07, (0, 3): -0.04, (1, 2): 0.06, (1, 3): 0.05, (2, 3): -0.03}
+
+    def pot_fn(p, t):
+        out = 0.5 * (p * p).sum(axis=-1) + 0.01 * (p ** 4).sum(axis=-1)
+        for (a, b), c in cij.items():
+            out = out + c * p[:, a] * p[:, b]
+        return out
+
+    w = W.CONFIGS["cfg4"].scaled(15, "cfg4g")
+    c = W.coefficients(w)
+    full = hp.build_full(w.dim, w.bound)
+    pot = hp.custom_potential(pot_fn, w.dim, W.HALFWIDTH)
+    scheme = hp.MagnusScheme.from_name("midpoint")
+    want = hp.FastHamiltonian(full, pot, w.degree).propagate(scheme, torch.from_numpy(c).cuda(), 0.0, w.dt, 2, 7)
+    shards = [SlabShard(w.dim, w.bound, r, 3, halo=w.degree) for r in range(3)]
+    ys = []
+    for s in shards:
+        g = s.geo
+        y = torch.zeros(g.box_size, dtype=torch.complex128, device="cuda")
+        y[g.own_slice] = torch.from_numpy(c[g.lo * g.plane:g.hi * g.plane]).cuda()
+        ys.append(y)
+    fh = hp.FastHamiltonian(full, pot, w.degree)
+    sharded_propagate(shards, fh, ys, 0.0, w.dt, 2, 7, reduce=local_sum, exchange=emulate_exchange)
+    got = torch.cat([y[s.geo.own_slice] for s, y in zip(shards, ys)])
+    assert float(torch.linalg.vector_norm(got - want) / torch.linalg.vector_norm(want)) < 1e-12
+
+
 def test_lincomb_entry_points():
     """hp_lincomb3_nrm2sq / hp_lincomb (the sharded Lanczos update and combine) against numpy."""
     import ctypes
