@@ -13,11 +13,14 @@
 // device and structure.  Everything here is optional: if NVRTC or the driver entry points are
 // missing, or a compilation fails, level_apply launches the interpreted kernel instead.
 #include <dlfcn.h>
+#include <unistd.h>
 #include <nvrtc.h>
 #include <cuda.h>
 
 #include <atomic>
 #include <cctype>
+#include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -182,8 +185,39 @@ int spill_bytes(const std::string& log) {
 }
 
 // NVRTC: source -> cubin (no device needed); *spills = bytes ptxas spilled
+// Optional cubin cache on disk (HP_LEVEL_JIT_CACHE=<dir>, off by default: no hidden state): one
+// file per (source, launch bounds, options) holding the spill count and the cubin, so a structure
+// is compiled once per machine instead of once per process.
+std::string cache_path(const std::string& src, const std::string& opts) {
+  const char* dir = getenv("HP_LEVEL_JIT_CACHE");
+  if (!dir || !*dir) return std::string();
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over options and source
+  for (const std::string* s : {&opts, &src})
+    for (unsigned char c : *s) h = (h ^ c) * 1099511628211ull;
+  char name[64];
+  snprintf(name, sizeof name, "/hp_level_%016llx_%zu.cubin", (unsigned long long)h, src.size());
+  return std::string(dir) + name;
+}
+
 bool compile_cubin(const std::string& src, int minb, int* spills, std::vector<char>* cubin) {
   const Rtc& r = rtc();
+  const char* defs = getenv("HP_LEVEL_JIT_DEFS");
+  const std::string path = cache_path(src, "sm_100a minb=" + std::to_string(minb) + " " + (defs ? defs : ""));
+  if (!path.empty())
+    if (FILE* f = fopen(path.c_str(), "rb")) {
+      int sp = 0;
+      uint64_t n = 0;
+      bool ok = fread(&sp, sizeof sp, 1, f) == 1 && fread(&n, sizeof n, 1, f) == 1 && n > 0 && n < (64u << 20);
+      if (ok) {
+        cubin->resize(n);
+        ok = fread(cubin->data(), 1, n, f) == n;
+      }
+      fclose(f);
+      if (ok) {
+        *spills = sp;
+        return true;
+      }
+    }
   nvrtcProgram prog = nullptr;
   if (r.create(&prog, src.c_str(), "hp_level_gen.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return false;
   const std::string bounds = "-DLV_MINB=" + std::to_string(minb);
@@ -205,6 +239,16 @@ bool compile_cubin(const std::string& src, int minb, int* spills, std::vector<ch
     ok = r.cubin(prog, cubin->data()) == NVRTC_SUCCESS;
   }
   r.destroy(&prog);
+  if (ok && !path.empty()) {  // written under a temporary name, then renamed: readers never see a partial file
+    const std::string tmp = path + ".tmp" + std::to_string((long)getpid());
+    if (FILE* f = fopen(tmp.c_str(), "wb")) {
+      const uint64_t n = cubin->size();
+      const bool w = fwrite(spills, sizeof *spills, 1, f) == 1 && fwrite(&n, sizeof n, 1, f) == 1 &&
+                     fwrite(cubin->data(), 1, n, f) == n;
+      fclose(f);
+      if (!w || rename(tmp.c_str(), path.c_str()) != 0) remove(tmp.c_str());
+    }
+  }
   return ok;
 }
 
