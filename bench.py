@@ -385,8 +385,13 @@ def gpu_arm(args, rank, world, local_rank):
     # owned planes (it writes only those), a batch rank its own vectors, a replica the whole set
     alg_bytes = 32.0 * total_coeffs / world
     achieved = alg_bytes / (ms_step * 1e-3) / 1e9
+    traffic, traffic_source = profiled_traffic(args.workload), "committed ncu capture (profiles/traffic.json)"
+    if rank == 0 and world == 1 and not args.no_traffic:
+        live = measured_traffic(args.workload)
+        if live:
+            traffic, traffic_source = live, "ncu child process of this run, one matvec (after the timed region)"
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": profiled_traffic(args.workload),
+                "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_source": traffic_source,
                 "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg_bytes,
                 "basis": "one full matvec (all its kernels) per step; 32 B/coefficient; per GPU, max-over-ranks time"}
 
@@ -607,6 +612,47 @@ def profiled_traffic(workload: str):
     return _profile_record().get(workload)
 
 
+_MATVEC_KERNELS = ("k_fg_quad", "k_fg_single", "k_fg_pairs", "k_fg_combine", "k_fg_inner", "k_fg_outer", "k_level",
+                   "k_coord", "k_cheb", "k_axpy", "k_osc")
+
+
+def measured_traffic(workload: str, timeout_s: float = 240.0):
+    """DRAM bytes (read + write) of ONE matvec of `workload`, measured now: a child process runs
+    tools/prof_matvec.py (one matvec after set construction) under `ncu --metrics
+    dram__bytes_read.sum,dram__bytes_write.sum` and the matvec kernels' counts are summed.  After
+    the timed region, never inside it.  None when ncu is missing, fails or exceeds the timeout
+    (the committed capture is reported then)."""
+    import csv
+    import shutil
+    import tempfile
+
+    if shutil.which("ncu") is None:
+        return None
+    with tempfile.TemporaryDirectory() as td:
+        log = Path(td) / "traffic.csv"
+        cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none", "--csv",
+               "--log-file", str(log), sys.executable, str(ROOT / "tools" / "prof_matvec.py"), workload, "1"]
+        try:
+            r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout_s)
+        except (subprocess.TimeoutExpired, OSError):
+            return None
+        if r.returncode != 0 or not log.exists():
+            return None
+        rows = list(csv.reader(ln for ln in log.read_text().splitlines() if ln.startswith('"')))
+    if not rows or "Kernel Name" not in rows[0]:
+        return None
+    hdr = rows[0]
+    ki, mi, ui, vi = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Unit", "Metric Value"))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    total, seen = 0.0, False
+    for row in rows[1:]:
+        if not row[mi].startswith("dram__bytes") or not any(k in row[ki] for k in _MATVEC_KERNELS):
+            continue
+        total += float(row[vi].replace(",", "")) * scale.get(row[ui], 1.0)
+        seen = True
+    return int(total) if seen else None
+
+
 def fp64_utilisation(workload: str, ms_step: float):
     """FP64 rate of the step against the measured DFMA peak: the step's FP64 flops are the ncu
     instruction counts of its kernels (committed with the capture; the kernels' flop count per
@@ -655,6 +701,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-reps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="report the committed DRAM-traffic capture instead of measuring one matvec under ncu")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--mode", default="matvec", choices=["matvec", "step"],
                     help="step: the named propagation run (cfg1/cfg3/cfg4) is the headline metric")
