@@ -386,10 +386,12 @@ def gpu_arm(args, rank, world, local_rank):
     alg_bytes = 32.0 * total_coeffs / world
     achieved = alg_bytes / (ms_step * 1e-3) / 1e9
     traffic, traffic_source = profiled_traffic(args.workload), "committed ncu capture (profiles/traffic.json)"
+    live_flops = None
     if rank == 0 and world == 1 and not args.no_traffic:
         live = measured_traffic(args.workload)
         if live:
-            traffic, traffic_source = live, "ncu child process of this run, one matvec (after the timed region)"
+            traffic, traffic_source = live[0], "ncu child process of this run, one matvec (after the timed region)"
+            live_flops = live[1]
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_source": traffic_source,
                 "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg_bytes,
@@ -473,7 +475,7 @@ def gpu_arm(args, rank, world, local_rank):
                                            f"skipped, {sharding.schedule()} schedule; value = that rank's planes/s)")
                            if emu else f"slab-j1 x{world}" if sharding is not None else
                            ("single" if world == 1 else f"batch/{world}" if part else f"replicas x{world}")},
-                "roofline": roofline, "fp64": fp64_utilisation(w.name, ms_step) if not emu and world == 1 else None,
+                "roofline": roofline, "fp64": fp64_utilisation(w.name, ms_step, live_flops) if not emu and world == 1 else None,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "specialised_level_kernels": int(nat.lib().hp_level_jit_kernels()),
                 "clocks": clk.summary(), "propagation": prop}
@@ -617,11 +619,12 @@ _MATVEC_KERNELS = ("k_fg_quad", "k_fg_single", "k_fg_pairs", "k_fg_combine", "k_
 
 
 def measured_traffic(workload: str, timeout_s: float = 240.0):
-    """DRAM bytes (read + write) of ONE matvec of `workload`, measured now: a child process runs
+    """(DRAM bytes read + written, FP64 flops) of ONE matvec of `workload`, measured now: a child process runs
     tools/prof_matvec.py (one matvec after set construction) under `ncu --metrics
-    dram__bytes_read.sum,dram__bytes_write.sum` and the matvec kernels' counts are summed.  After
-    the timed region, never inside it.  None when ncu is missing, fails or exceeds the timeout
-    (the committed capture is reported then)."""
+    dram__bytes_read.sum,dram__bytes_write.sum` (and the dfma / dadd / dmul thread-instruction
+    counts: flops = 2 dfma + dadd + dmul) and the matvec kernels' counts are summed.  After the
+    timed region, never inside it.  None when ncu is missing, fails or exceeds the timeout (the
+    committed capture is reported then)."""
     import csv
     import shutil
     import tempfile
@@ -630,7 +633,9 @@ def measured_traffic(workload: str, timeout_s: float = 240.0):
         return None
     with tempfile.TemporaryDirectory() as td:
         log = Path(td) / "traffic.csv"
-        cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none", "--csv",
+        fp = "smsp__sass_thread_inst_executed_op_%s_pred_on.sum"
+        cmd = ["ncu", "--metrics", ",".join(["dram__bytes_read.sum", "dram__bytes_write.sum"] + [fp % o for o in ("dfma", "dadd", "dmul")]),
+               "--clock-control", "none", "--csv",
                "--log-file", str(log), sys.executable, str(ROOT / "tools" / "prof_matvec.py"), workload, "1"]
         try:
             r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout_s)
@@ -644,28 +649,36 @@ def measured_traffic(workload: str, timeout_s: float = 240.0):
     hdr = rows[0]
     ki, mi, ui, vi = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Unit", "Metric Value"))
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-    total, seen = 0.0, False
+    total, flops, seen = 0.0, 0.0, False
     for row in rows[1:]:
-        if not row[mi].startswith("dram__bytes") or not any(k in row[ki] for k in _MATVEC_KERNELS):
+        if not any(k in row[ki] for k in _MATVEC_KERNELS):
             continue
-        total += float(row[vi].replace(",", "")) * scale.get(row[ui], 1.0)
-        seen = True
-    return int(total) if seen else None
+        val = float(row[vi].replace(",", ""))
+        if row[mi].startswith("dram__bytes"):
+            total += val * scale.get(row[ui], 1.0)
+            seen = True
+        elif "_op_dfma_" in row[mi]:
+            flops += 2.0 * val
+        elif "_op_dadd_" in row[mi] or "_op_dmul_" in row[mi]:
+            flops += val
+    return (int(total), int(flops)) if seen else None
 
 
-def fp64_utilisation(workload: str, ms_step: float):
+def fp64_utilisation(workload: str, ms_step: float, live_flops=None):
     """FP64 rate of the step against the measured DFMA peak: the step's FP64 flops are the ncu
     instruction counts of its kernels (committed with the capture; the kernels' flop count per
     matvec is fixed by the term list, not by the run), divided by this run's step time."""
     rec = _profile_record()
-    flops = (rec.get("fp64_flops") or {}).get(workload)
+    flops = live_flops or (rec.get("fp64_flops") or {}).get(workload)
     peak = rec.get("fp64_peak_tflops")
     if not flops or not peak:
         return None
     ach = flops / (ms_step * 1e-3) / 1e12
     return {"flops_per_step": flops, "achieved_tflops": round(ach, 3), "peak_tflops": peak,
             "frac": round(ach / peak, 4), "peak_kind": "measured (tools/microbench.cu DFMA chain)",
-            "source": "ncu 2 x dfma + dadd + dmul thread instructions of the step's kernels (profiles/traffic.json)"}
+            "source": "ncu 2 x dfma + dadd + dmul thread instructions of the step's kernels ("
+                      + ("counted in this run, same ncu child process as roofline.traffic" if live_flops
+                         else "profiles/traffic.json") + ")"}
 
 
 def step_mode(args, w, rank, world, local_rank, hbm, peak_kind):
