@@ -302,8 +302,11 @@ bool level_jit_enabled(int64_t work) {
 #else
   const char* e = getenv("HP_LEVEL_JIT");
   if (e && !atoi(e)) return false;
-  const char* m = getenv("HP_LEVEL_JIT_MIN");  // smallest n * batch worth a compilation (~0.4 s per level)
-  const int64_t min_work = m ? atoll(m) : ((int64_t)1 << 22);
+  // smallest n * batch worth a compilation (~0.4 s per level and process); with the on-disk cache
+  // the compilation is paid once per machine, so mid-sized sets are specialised too
+  const char* m = getenv("HP_LEVEL_JIT_MIN");
+  const char* cache = getenv("HP_LEVEL_JIT_CACHE");
+  const int64_t min_work = m ? atoll(m) : ((int64_t)1 << (cache && *cache ? 17 : 22));
   return work >= min_work && rtc().ok;
 #endif
 }
