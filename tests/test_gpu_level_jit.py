@@ -115,3 +115,39 @@ def test_fallback_when_specialisation_is_off(hp, monkeypatch):
     v = np.random.default_rng(3).standard_normal(s.size) + 0j
     y = hp.get_applier(s).apply_polynomial(_approx(degs, coeffs, 3, 3), v)
     assert rel_l2(y, oa.polynomial(degs, coeffs, 16.0, v)) < TOL
+
+
+def test_on_disk_kernel_cache(hp, tmp_path, monkeypatch):
+    """HP_LEVEL_JIT_CACHE: compiled kernels are written to the directory and a second process
+    loads them (same results, nothing recompiled: its run is much shorter than the first)."""
+    import os
+    import subprocess
+    import sys
+    import time
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    script = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {str(root)!r})\n"
+        "import paper_1403_3511_b200 as hp\n"
+        "from paper_1403_3511_b200 import _native as nat, workloads as W\n"
+        "w = W.CONFIGS['cfg5'].scaled(31, 'cfg5c')\n"
+        "s = hp.build_hyperbolic(w.dim, w.bound)\n"
+        "c = W.coefficients(w, s.indices)\n"
+        "y = hp.get_applier(s).apply_polynomial(w.approx(0.0), c)\n"
+        "np.save(sys.argv[1], y)\n"
+        "print(nat.lib().hp_level_jit_kernels())\n")
+    env = {**os.environ, "HP_LEVEL_JIT_CACHE": str(tmp_path), "HP_LEVEL_JIT_MIN": "0"}
+    outs, walls, counts = [], [], []
+    for i in range(2):
+        f = tmp_path / f"y{i}.npy"
+        t0 = time.time()
+        r = subprocess.run([sys.executable, "-c", script, str(f)], env=env, capture_output=True, text=True, timeout=600)
+        walls.append(time.time() - t0)
+        assert r.returncode == 0, r.stderr[-2000:]
+        counts.append(int(r.stdout.strip().splitlines()[-1]))
+        outs.append(np.load(f))
+    assert counts[0] > 0 and counts[1] == counts[0]
+    assert len(list(tmp_path.glob("hp_level_*.cubin"))) >= counts[0]
+    assert np.array_equal(outs[0], outs[1])
