@@ -149,6 +149,8 @@ struct hp_set_s {
   // sqrt(j / 2) for j = -8 .. bound + 8 (entry j at [j + 8]): the ladder coefficients of the level
   // kernels (hp_level.cu ladder_table); boxes and hyperbolic crosses only (indices <= bound)
   mutable double* d_sqtab = nullptr;
+  // tabled sets: sum_l j_l per ordinal, the oscillator levels of apply_hamiltonian (hp_level.cu level_sums)
+  mutable int32_t* d_jsum = nullptr;
 
   hp::AxBox box(int a) const {
     hp::AxBox v;

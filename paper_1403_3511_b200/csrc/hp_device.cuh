@@ -427,9 +427,7 @@ __device__ __forceinline__ void lv_body(int64_t n, int64_t batch, const AX& ax, 
         R[k][p] = a;
       }
     }
-    double lev = 0.0;
-    if (osc)
-      for (int a = 0; a < dim; ++a) lev += (double)axs.j(a, o) + 0.5;
+    const double lev = osc ? axs.level(dim, o) : 0.0;  // oscillator level sum_l (j_l + 1/2)
     for (int64_t b = 0; b < batch; ++b) {
       const int64_t bo = b * n;
       double2 accs[TGN];
@@ -484,13 +482,26 @@ struct LvAllBox {
 #endif
   AxBox ax[HP_MAXDIM];
   __device__ __forceinline__ int j(int a, int64_t o) const { return ax[a].jloc(o) + ax[a].joff; }
+  __device__ __forceinline__ double level(int dim, int64_t o) const {
+    double lev = 0.0;
+    for (int a = 0; a < dim; ++a) lev += (double)j(a, o) + 0.5;
+    return lev;
+  }
 };
 struct LvAllTab {
 #ifndef __CUDACC_RTC__
   static const char* name() { return "hp::LvAllTab"; }  // type name in runtime-compiled source
 #endif
   AxTab ax[HP_MAXDIM];
+  const int32_t* jsum;  // sum_l j_l per ordinal (hp_level.cu level_sums), or null
   __device__ __forceinline__ int j(int a, int64_t o) const { return __ldg(ax[a].jv + o); }
+  // sum_l (j_l + 1/2): exact in double either way; one 4-byte load instead of one per axis
+  __device__ __forceinline__ double level(int dim, int64_t o) const {
+    if (jsum) return (double)__ldg(jsum + o) + 0.5 * dim;
+    double lev = 0.0;
+    for (int a = 0; a < dim; ++a) lev += (double)j(a, o) + 0.5;
+    return lev;
+  }
 };
 
 

@@ -483,6 +483,8 @@ static hp_status window_table(const hp_set_s* s, int a, int K, cudaStream_t st, 
   return HP_OK;
 }
 
+static hp_status level_sums(const hp_set_s* s, cudaStream_t st, const int32_t** out);
+
 // hp_level_jit.cu
 bool level_jit_enabled(int64_t work);
 bool level_jit_launch(int device, const char* ax_name, const void* ax, const char* axs_name, const void* axs,
@@ -528,6 +530,9 @@ static hp_status launch_level(const hp_set_s* s, const LvLevel& lv, double L, co
   } else {
     LvAllTab axs;
     for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
+    axs.jsum = nullptr;
+    if (osc)
+      if (hp_status rc = level_sums(s, st, &axs.jsum)) return rc;
     int kwin = 0;
     const int32_t* win = nullptr;
     if (lv.axis == s->dim - 1 && !perm && s->kind == HP_KIND_HYPERBOLIC) {
@@ -578,6 +583,36 @@ static hp_status ladder_table(const hp_set_s* s, cudaStream_t st, const double**
     s->d_sqtab = t;
   }
   *out = s->d_sqtab + 8;
+  return HP_OK;
+}
+
+// ---------------------------------------------------------------- oscillator levels
+
+__global__ void k_level_sums(int64_t n, int dim, LvAllTab axs, int32_t* __restrict__ out) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+    int sum = 0;
+    for (int a = 0; a < dim; ++a) sum += axs.j(a, o);
+    out[o] = sum;
+  }
+}
+
+// sum_l j_l per ordinal of a tabled set, built once: the level that adds the oscillator diagonal
+// (apply_hamiltonian, fast_apply.py:195-198) then loads 4 bytes per ordinal instead of one j per axis
+static hp_status level_sums(const hp_set_s* s, cudaStream_t st, const int32_t** out) {
+  *out = nullptr;
+  if (s->boxed || s->n < 1) return HP_OK;
+  std::lock_guard<std::mutex> g(s->perm_mtx);
+  if (!s->d_jsum) {
+    int32_t* t = nullptr;
+    HP_CUDA(cudaMalloc(&t, (size_t)s->n * sizeof(int32_t)));
+    LvAllTab axs;
+    for (int a = 0; a < s->dim; ++a) axs.ax[a] = s->tab(a);
+    axs.jsum = nullptr;
+    k_level_sums<<<grid_for(s->n, 256), 256, 0, st>>>(s->n, s->dim, axs, t);
+    HP_LAUNCH_CHECK("k_level_sums");
+    s->d_jsum = t;
+  }
+  *out = s->d_jsum;
   return HP_OK;
 }
 

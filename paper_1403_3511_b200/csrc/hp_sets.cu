@@ -501,6 +501,7 @@ hp_status hp_set_destroy(hp_set_t s) {
     if (s->d_win[a]) cudaFree(s->d_win[a]);
   }
   if (s->d_sqtab) cudaFree(s->d_sqtab);
+  if (s->d_jsum) cudaFree(s->d_jsum);
   if (s->d_pref) cudaFree(s->d_pref);
   if (s->d_off) cudaFree(s->d_off);
   if (s->fg_basis) cudaFree(s->fg_basis);
